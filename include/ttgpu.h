@@ -1,0 +1,161 @@
+/* ttgpu — C ABI of the B200 (sm_100a) MPO·MPS apply / Hadamard + canonical
+ * simplification hot path.
+ *
+ * This is the boundary the drop-in C++ headers (include/ttlab/*.hpp) call in
+ * place of the reference's Eigen implementation.  Every entry point names the
+ * reference function it replaces (paths relative to
+ * /root/reference/proj/include/ttlab/).  Plain C types only: pointers, sizes,
+ * integers and doubles.
+ *
+ * Conventions
+ *   - Tensors are row-major, Tensor3 A[left, phys, right] (tensor.hpp:13-86) and
+ *     Tensor4 B[left, out, in, right] (tensor.hpp:89-149).  dtype TTG_F64 holds
+ *     doubles, TTG_C128 interleaved (re, im) pairs = std::complex<double>.
+ *   - A ttg_dmps is a device-resident batch of `count` chains with identical
+ *     length and physical dimensions (count = 1 for an ordinary MPS).
+ *   - Every call returns a ttg_status; on failure ttg_last_error(ctx) holds the
+ *     message.  TTG_SHAPE / TTG_CAPACITY / TTG_NUMERIC map to the reference's
+ *     shape_error / capacity_error / numeric_error (types.hpp:22-37).
+ *   - One context per host thread; calls are stream-ordered on the context's
+ *     stream and synchronous at return unless documented otherwise.
+ */
+#ifndef TTGPU_H
+#define TTGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  TTG_OK = 0,
+  TTG_SHAPE = 1,    /* shape_error   (types.hpp:22-25) */
+  TTG_CAPACITY = 2, /* capacity_error (types.hpp:28-31) */
+  TTG_NUMERIC = 3,  /* numeric_error (types.hpp:34-37) */
+  TTG_CUDA = 4,     /* CUDA runtime failure / no device */
+  TTG_INVALID = 5   /* bad argument (null pointer, unknown dtype, ...) */
+} ttg_status;
+
+typedef enum { TTG_F64 = 0, TTG_C128 = 1 } ttg_dtype;
+typedef enum { TTG_SVD_TRUNCATE = 0, TTG_VARIATIONAL = 1 } ttg_truncation; /* types.hpp:39 */
+
+/* types.hpp:50-88 Strategy.  max_bond <= 0 or >= INT32_MAX means unbounded. */
+typedef struct {
+  int method;
+  double tolerance;
+  double simplification_tolerance;
+  int64_t max_bond;
+  int max_sweeps;
+  int normalize;
+} ttg_strategy;
+
+/* Per-chain outcome of simplify / apply (simplify.hpp:94-99 CompressionResult). */
+typedef struct {
+  int sweeps;
+  int converged;
+  double residual;     /* sqrt(dist2) + fp_error_floor(|T|)   (simplify.hpp:126) */
+  double error;        /* error ledger of the output state      (simplify.hpp:191) */
+  double norm;         /* |psi| = Frobenius norm of the centre  (mps.hpp:225)      */
+  double target_norm2; /* <T, T>                                (simplify.hpp:37-41) */
+} ttg_report;
+
+/* Host view of one MPS (mps.hpp:21-143): n sites, bonds[n+1], phys[n],
+ * sites[k] -> bonds[k]*phys[k]*bonds[k+1] elements of `dtype`. */
+typedef struct {
+  int n;
+  int dtype;
+  const int64_t* bonds;
+  const int64_t* phys;
+  const void* const* sites;
+  double error;
+} ttg_mps_view;
+
+/* Host view of one MPO (mpo.hpp:14-105): sites[k] -> bonds[k]*out[k]*in[k]*bonds[k+1]. */
+typedef struct {
+  int n;
+  int dtype;
+  const int64_t* bonds;
+  const int64_t* phys_out;
+  const int64_t* phys_in;
+  const void* const* sites;
+} ttg_mpo_view;
+
+typedef struct ttg_ctx ttg_ctx;
+typedef struct ttg_dmps ttg_dmps;
+typedef struct ttg_dmpo ttg_dmpo;
+
+/* ---- context ------------------------------------------------------------ */
+ttg_status ttg_create(int device, ttg_ctx** out);
+void ttg_destroy(ttg_ctx* ctx);
+const char* ttg_last_error(const ttg_ctx* ctx);
+/* Run on an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+ttg_status ttg_set_stream(ttg_ctx* ctx, void* cuda_stream);
+ttg_status ttg_synchronize(ttg_ctx* ctx);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t ttg_kernel_launches(const ttg_ctx* ctx);
+const char* ttg_version(void);
+
+/* ---- device MPS / MPO ---------------------------------------------------- */
+/* Upload `count` host MPS of identical length/physical dims/bonds as one batch. */
+ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, ttg_dmps** out);
+/* Wrap device-resident site tensors (copied, stream-ordered):
+ * dev_sites[k] holds count * bonds[k]*phys[k]*bonds[k+1] contiguous elements. */
+ttg_status ttg_mps_from_device(ttg_ctx* ctx, int n, int dtype, int count, const int64_t* bonds,
+                               const int64_t* phys, const void* const* dev_sites, const double* errors,
+                               ttg_dmps** out);
+void ttg_mps_free(ttg_dmps* m);
+/* Shape of chain `chain`: n, dtype, count, bonds[n+1], phys[n], error, centre (-1 if not canonical). */
+ttg_status ttg_mps_info(const ttg_dmps* m, int chain, int* n, int* dtype, int* count, int64_t* bonds, int64_t* phys,
+                        double* error, int* center);
+/* Copy chain `chain` to caller-allocated host buffers sized from ttg_mps_info. */
+ttg_status ttg_mps_download(ttg_ctx* ctx, const ttg_dmps* m, int chain, void* const* sites);
+/* Device pointer of site k of chain `chain` and its element count (for zero-copy readers). */
+ttg_status ttg_mps_site_ptr(const ttg_dmps* m, int chain, int k, void** ptr, int64_t* elems);
+
+ttg_status ttg_mpo_upload(ttg_ctx* ctx, const ttg_mpo_view* view, ttg_dmpo** out);
+void ttg_mpo_free(ttg_dmpo* w);
+
+/* ---- hot path ------------------------------------------------------------- */
+/* mpo.hpp:213-238 detail::apply_raw — exact MPO·MPS, fused bond (mpo, mps). */
+ttg_status ttg_apply_raw(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, ttg_dmps** out);
+/* blas.hpp:45-67 hadamard — exact element-wise product, bonds multiply. */
+ttg_status ttg_hadamard(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, ttg_dmps** out);
+/* simplify.hpp:182-195 simplify(MPS, Strategy, optional guess); guess may be NULL.
+ * Returns a canonical batch (centre 0); reports[count] may be NULL. */
+ttg_status ttg_simplify(ttg_ctx* ctx, const ttg_dmps* target, const ttg_strategy* strategy, const ttg_dmps* guess,
+                        ttg_dmps** out, ttg_report* reports);
+/* blas.hpp:8-11 apply(MPO, MPS, Strategy) = simplify(apply_raw(op, v)). */
+ttg_status ttg_apply(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, const ttg_strategy* strategy,
+                     ttg_dmps** out, ttg_report* reports);
+/* mps.hpp:310-313 canonicalize(MPS, centre, Strategy) (QR pass + truncating sweep). */
+ttg_status ttg_canonicalize(ttg_ctx* ctx, const ttg_dmps* v, int center, const ttg_strategy* strategy,
+                            ttg_dmps** out, ttg_report* reports);
+/* mps.hpp:416-423 scprod(u, v) per chain: out_re/out_im[count]. */
+ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double* out_re, double* out_im);
+
+/* ---- kernel-level test hooks (host buffers; one kernel each) ------------- */
+/* C[b] = op(A[b]) op(B[b]) for b < batch; op: 0 = N, 1 = T, 2 = C (conj-transpose), 3 = conj. */
+ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A, const void* B,
+                          void* C);
+/* schmidt_split (schmidt.hpp:72-89) of one m x n theta: mode 0 = LEFT_TO_RIGHT writes U_r (m x r),
+ * mode 1 = RIGHT_TO_LEFT writes V_r^H (r x n); svals[min(m,n)] descending, rank, dropped weight^2. */
+ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
+                         void* iso, double* svals, int* rank, double* err2);
+/* Thin Householder QR (mps.hpp:196-199): Q (m x k), R (k x n), k = min(m, n). */
+ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTGPU_H */

@@ -1,0 +1,126 @@
+// Kernel-level test hooks of the C ABI (host buffers in, host buffers out).
+// They run exactly the kernels the engine uses, one call each, so the parity
+// tests can pin the GEMM fragment layouts, the QR and the truncated SVD in
+// isolation before the sweep engine is involved.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ttgpu.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "jacobi_svd.cuh"
+#include "qr.cuh"
+
+using namespace ttg;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  explicit Buf(size_t bytes) { cudaMalloc(&p, bytes ? bytes : 16); }
+  ~Buf() { cudaFree(p); }
+};
+
+ttg_status cuda_status(cudaError_t e) { return e == cudaSuccess ? TTG_OK : TTG_CUDA; }
+
+template <typename T>
+ttg_status do_gemm(int opA, int opB, int M, int N, int K, const void* A, const void* B, void* Cout, int batch) {
+  const size_t es = sizeof(T);
+  const size_t na = (size_t)M * K, nb = (size_t)K * N, nc = (size_t)M * N;
+  Buf a(na * es * batch), b(nb * es * batch), c(nc * es * batch);
+  cudaMemcpy(a.p, A, na * es * batch, cudaMemcpyHostToDevice);
+  cudaMemcpy(b.p, B, nb * es * batch, cudaMemcpyHostToDevice);
+  GemmParams p{a.p, b.p, c.p, (long long)na, (long long)nb, (long long)nc, dconst(M), dconst(N), dconst(K),
+               nullptr, 0, nullptr, 1.0, 0};
+  cudaError_t e = gemm<T>(p, opA, opB, M, N, batch, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(Cout, c.p, nc * es * batch, cudaMemcpyDeviceToHost);
+  return cuda_status(e);
+}
+
+template <typename T>
+ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t max_bond, void* iso, double* svals,
+                  int* rank, double* err2) {
+  const size_t es = sizeof(T);
+  const int kmin = m < n ? m : n;
+  Buf th((size_t)m * n * es), is((size_t)m * n * es + (size_t)kmin * kmin * es), sv((size_t)kmin * 8),
+      bonds(4 * sizeof(int)), st(sizeof(ChainState)), work((size_t)m * n * es);
+  cudaMemcpy(th.p, theta, (size_t)m * n * es, cudaMemcpyHostToDevice);
+  ChainState z{};
+  z.active = 1;
+  cudaMemcpy(st.p, &z, sizeof z, cudaMemcpyHostToDevice);
+  int hb[4] = {m, n, 0, 0};
+  cudaMemcpy(bonds.p, hb, sizeof hb, cudaMemcpyHostToDevice);
+  SvdParams p{};
+  p.theta = th.p;
+  p.M = dbond(0);
+  p.N = dbond(1);
+  p.bonds = static_cast<int*>(bonds.p);
+  p.ld = 4;
+  p.out_idx = 2;
+  p.iso = is.p;
+  p.svals = static_cast<double*>(sv.p);
+  p.st = static_cast<ChainState*>(st.p);
+  p.check_active = 0;
+  p.accumulate_err = 1;
+  p.tol = tol;
+  p.max_bond = max_bond;
+  p.mode = mode;
+  p.work = work.p;
+  const int l = mode == 0 ? m : n, k = mode == 0 ? n : m;
+  cudaError_t e = jacobi_svd<T>(p, l, k, 1, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return TTG_CUDA;
+  cudaMemcpy(hb, bonds.p, sizeof hb, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&z, st.p, sizeof z, cudaMemcpyDeviceToHost);
+  const int r = hb[2];
+  *rank = r;
+  *err2 = z.err2;
+  cudaMemcpy(svals, sv.p, (size_t)kmin * 8, cudaMemcpyDeviceToHost);
+  const size_t iso_elems = mode == 0 ? (size_t)m * r : (size_t)r * n;
+  cudaMemcpy(iso, is.p, iso_elems * es, cudaMemcpyDeviceToHost);
+  if (z.status) return TTG_NUMERIC;
+  return TTG_OK;
+}
+
+template <typename T>
+ttg_status do_qr(int m, int n, const void* A, void* Q, void* R) {
+  const size_t es = sizeof(T);
+  const int k = m < n ? m : n;
+  Buf a((size_t)m * n * es), q((size_t)m * k * es), r((size_t)k * n * es),
+      w(qr_workspace_elems<T>(m, n) * es);
+  cudaMemcpy(a.p, A, (size_t)m * n * es, cudaMemcpyHostToDevice);
+  QrParams p{a.p, 0, q.p, 0, r.p, 0, w.p, 0, m, n};
+  cudaError_t e = householder_qr<T>(p, 1, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return TTG_CUDA;
+  cudaMemcpy(Q, q.p, (size_t)m * k * es, cudaMemcpyDeviceToHost);
+  cudaMemcpy(R, r.p, (size_t)k * n * es, cudaMemcpyDeviceToHost);
+  return TTG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A, const void* B,
+                          void* C) {
+  if (M < 1 || N < 1 || K < 0 || batch < 1) return TTG_INVALID;
+  return dtype == TTG_F64 ? do_gemm<double>(opA, opB, M, N, K, A, B, C, batch)
+                          : do_gemm<cplx>(opA, opB, M, N, K, A, B, C, batch);
+}
+
+ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
+                         void* iso, double* svals, int* rank, double* err2) {
+  if (m < 1 || n < 1) return TTG_INVALID;
+  return dtype == TTG_F64 ? do_svd<double>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2)
+                          : do_svd<cplx>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2);
+}
+
+ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R) {
+  if (m < 1 || n < 1) return TTG_INVALID;
+  return dtype == TTG_F64 ? do_qr<double>(m, n, A, Q, R) : do_qr<cplx>(m, n, A, Q, R);
+}
+
+}  // extern "C"

@@ -1,0 +1,1022 @@
+// Host side of the ttgpu C ABI: device MPS/MPO containers and the sweep
+// engine that drives the sm_100a kernels.
+//
+// The engine restates, for a batch of independent chains with one shared
+// shape, the reference's
+//   CanonicalMPS(const MPS&, center, Strategy)      mps.hpp:188-218
+//   CompressionEngine + variational_compress         simplify.hpp:15-131
+//   simplify(MPS, Strategy, guess)                  simplify.hpp:182-195
+// Every truncation rank is produced on the device and written into a per-chain
+// bond table that the following kernels read, so the host never waits inside a
+// call: a whole simplify is one stream-ordered sequence of launches, with one
+// host read of the per-chain "active" flags per sweep (early stop) and one at
+// the end.
+#include <algorithm>
+#include <cstddef>
+#include <memory>
+#include <type_traits>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/ttgpu.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "jacobi_svd.cuh"
+#include "kernels.cuh"
+#include "qr.cuh"
+
+using namespace ttg;
+
+struct ttg_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+};
+
+struct ttg_dmps {
+  int n = 0, dtype = TTG_F64, count = 1;
+  std::vector<int> phys;          // n
+  std::vector<int> bonds;         // count * (n + 1), host mirror
+  std::vector<long long> cap;     // elements per chain per site
+  std::vector<void*> site;        // n device buffers of count * cap[k] elements
+  std::vector<double> error;      // per chain
+  int center = -1;
+  cudaStream_t stream = nullptr;  // allocation stream
+  ~ttg_dmps() {
+    for (void* p : site)
+      if (p) cudaFreeAsync(p, stream);
+  }
+  int bond(int chain, int k) const { return bonds[(size_t)chain * (n + 1) + k]; }
+  bool uniform() const {
+    for (int c = 1; c < count; ++c)
+      for (int k = 0; k <= n; ++k)
+        if (bond(c, k) != bond(0, k)) return false;
+    return true;
+  }
+};
+
+struct ttg_dmpo {
+  int n = 0, dtype = TTG_F64;
+  std::vector<int> bonds, dout, din;
+  std::vector<void*> site;
+  cudaStream_t stream = nullptr;
+  ~ttg_dmpo() {
+    for (void* p : site)
+      if (p) cudaFreeAsync(p, stream);
+  }
+};
+
+namespace {
+
+struct Error {
+  ttg_status st;
+  std::string msg;
+};
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) throw Error{TTG_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+size_t esize(int dtype) { return dtype == TTG_C128 ? 16 : 8; }
+
+// Stream-ordered device allocation (the default pool keeps freed blocks, so
+// repeated calls do not reach cudaMalloc).
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{TTG_CAPACITY, "device allocation of " + std::to_string(bytes) + " bytes failed"};
+    }
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(s, o.s);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{TTG_CAPACITY, "device allocation of " + std::to_string(bytes) + " bytes failed"};
+  }
+  return p;
+}
+
+ttg_dmps* new_dmps(int n, int dtype, int count, const std::vector<int>& phys, const std::vector<long long>& cap,
+                   cudaStream_t s) {
+  auto* m = new ttg_dmps();
+  m->n = n;
+  m->dtype = dtype;
+  m->count = count;
+  m->phys = phys;
+  m->cap = cap;
+  m->stream = s;
+  m->bonds.assign((size_t)count * (n + 1), 1);
+  m->error.assign(count, 0.0);
+  m->site.assign(n, nullptr);
+  try {
+    for (int k = 0; k < n; ++k) m->site[k] = dev_alloc((size_t)count * cap[k] * esize(dtype), s);
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  return m;
+}
+
+inline int clamp_bond(int64_t mb) {
+  if (mb <= 0 || mb >= std::numeric_limits<int>::max()) return std::numeric_limits<int>::max();
+  return (int)mb;
+}
+
+inline double fp_error_floor(double scale) { return 32.0 * std::numeric_limits<double>::epsilon() * scale; }
+
+// ---------------------------------------------------------------------------
+// sweep engine
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct Engine {
+  ttg_ctx* ctx;
+  cudaStream_t st;
+  int L, B;
+  std::vector<int> d, t, g, q, pb, bound;
+  int* d_bonds = nullptr;  // B x (L+1) psi bonds
+  int ld = 0;
+  ChainState* d_state = nullptr;
+
+  Engine(ttg_ctx* c, int L_, int B_) : ctx(c), st(c->stream), L(L_), B(B_) {}
+
+  int ub(DimExpr e) const { return e.idx < 0 ? e.mult : e.mult * bound[e.idx]; }
+
+  void G(const void* A, long long sA, const void* Bm, long long sB, void* C, long long sC, DimExpr M, DimExpr N,
+         DimExpr K, int opA, int opB, bool check_active, int beta = 0) {
+    GemmParams p{A, Bm, C, sA, sB, sC, M, N, K, d_bonds, ld, check_active ? d_state : nullptr, 1.0, beta};
+    CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st));
+    ++ctx->launches;
+  }
+
+  void S(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso, long long s_iso,
+         int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work) {
+    SvdParams p{};
+    p.theta = theta;
+    p.s_theta = s_theta;
+    p.M = M;
+    p.N = N;
+    p.bonds = d_bonds;
+    p.ld = ld;
+    p.out_idx = out_idx;
+    p.iso = iso;
+    p.s_iso = s_iso;
+    p.svals = nullptr;
+    p.s_svals = 0;
+    p.st = d_state;
+    p.check_active = check_active ? 1 : 0;
+    p.accumulate_err = accumulate ? 1 : 0;
+    p.tol = tol;
+    p.max_bond = max_bond == std::numeric_limits<int>::max() ? 0 : max_bond;
+    p.mode = mode;
+    p.work = work;
+    p.s_work = s_work;
+    const int m = ub(M), n = ub(N);
+    const int l = mode == 0 ? m : n, k = mode == 0 ? n : m;
+    CK(jacobi_svd<T>(p, l, k, B, st));
+    ++ctx->launches;
+  }
+};
+
+// Host-side bookkeeping shared by simplify / canonicalize.
+struct Plan {
+  std::vector<long long> psi_cap;
+  long long ccap = 1, rcap = 1, bcap = 1, svd_work = 0, qr_work = 0;
+  long long xz = 1, yw = 1, th = 1;
+  std::vector<long long> env_cap;
+};
+
+template <typename T>
+void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, const ttg_strategy& s,
+                  bool variational, int center, ttg_dmps** out, ttg_report* reports) {
+  const int L = target.n, B = target.count;
+  cudaStream_t st = ctx->stream;
+  Engine<T> E(ctx, L, B);
+  E.ld = L + 2;  // column L+1 is scratch (old bond during pass 3)
+  E.d = target.phys;
+  E.t.assign(target.bonds.begin(), target.bonds.begin() + (L + 1));
+  E.g.assign(guess.bonds.begin(), guess.bonds.begin() + (L + 1));
+  const int mb = clamp_bond(s.max_bond);
+  auto& d = E.d;
+  auto& t = E.t;
+  auto& g = E.g;
+  auto& q = E.q;
+  auto& pb = E.pb;
+  auto& bound = E.bound;
+  q.assign(L + 1, 1);
+  for (int k = 0; k + 1 < L; ++k) q[k + 1] = std::min((long long)q[k] * d[k], (long long)g[k + 1]);
+  q[L] = 1;
+  std::vector<long long> dl(L + 1, 1), dr(L + 1, 1);
+  const long long BIG = 1LL << 30;
+  for (int k = 1; k <= L; ++k) dl[k] = std::min(BIG, dl[k - 1] * d[k - 1]);
+  for (int k = L - 1; k >= 0; --k) dr[k] = std::min(BIG, dr[k + 1] * d[k]);
+  pb.assign(L + 2, 1);
+  bound.assign(L + 2, 1);
+  for (int k = 0; k <= L; ++k) {
+    pb[k] = (int)std::max(1LL, std::min({(long long)mb, dl[k], dr[k]}));
+    bound[k] = std::max(q[k], pb[k]);
+  }
+  pb[0] = pb[L] = bound[0] = bound[L] = 1;
+  bound[L + 1] = *std::max_element(bound.begin(), bound.end());
+
+  Plan P;
+  P.psi_cap.resize(L);
+  for (int k = 0; k < L; ++k) P.psi_cap[k] = (long long)bound[k] * d[k] * bound[k + 1];
+  for (int k = 0; k < L; ++k) {
+    const long long gk1 = g[k + 1];
+    P.ccap = std::max(P.ccap, (long long)q[k] * d[k] * std::max<long long>(gk1, bound[k + 1]));
+    if (k + 1 < L) {
+      P.rcap = std::max(P.rcap, (long long)q[k + 1] * gk1);
+      const long long qw = (long long)qr_workspace_elems<T>(q[k] * d[k], (int)gk1);
+      if (qw * (long long)sizeof(T) > 200 * 1024) P.qr_work = std::max(P.qr_work, qw);
+    }
+    P.bcap = std::max(P.bcap, (long long)q[k] * std::min<long long>(q[k], (long long)d[k] * bound[k + 1]));
+    P.bcap = std::max(P.bcap, (long long)bound[k + 1] * bound[k + 1]);
+    // R->L pass panels: theta = q_k x d p_{k+1}
+    const long long l1 = (long long)d[k] * bound[k + 1], k1 = q[k];
+    if ((l1 * k1) * (long long)sizeof(T) + k1 * 12 + 16 > 220 * 1024) P.svd_work = std::max(P.svd_work, l1 * k1);
+  }
+  for (int n = 0; n + 1 < L; ++n) {
+    const long long dn = d[n], dn1 = d[n + 1];
+    P.xz = std::max({P.xz, (long long)pb[n] * dn * t[n + 1], (long long)t[n + 1] * dn1 * pb[n + 2],
+                     (long long)t[n] * dn * pb[n + 1]});
+    P.yw = std::max({P.yw, (long long)pb[n] * dn * dn1 * t[n + 2], (long long)t[n] * dn * dn1 * pb[n + 2]});
+    P.th = std::max(P.th, (long long)pb[n] * dn * dn1 * pb[n + 2]);
+    const long long l = (long long)bound[n] * dn, kk = (long long)dn1 * bound[n + 2];
+    if (l * kk * (long long)sizeof(T) + std::max(l, kk) * 12 + 16 > 220 * 1024)
+      P.svd_work = std::max(P.svd_work, l * kk);
+  }
+  if (L >= 1) P.xz = std::max(P.xz, (long long)t[L - 1] * d[L - 1] * pb[L]);
+  P.env_cap.resize(L + 1);
+  for (int k = 0; k <= L; ++k) P.env_cap[k] = (long long)pb[k] * t[k];
+
+  // ---- output container and workspaces
+  ttg_dmps* psi = new_dmps(L, target.dtype, B, d, P.psi_cap, st);
+  std::unique_ptr<ttg_dmps> psi_guard(psi);
+  const size_t es = sizeof(T);
+  DevBuf bonds_buf((size_t)B * (L + 2) * sizeof(int), st);
+  DevBuf state_buf((size_t)B * sizeof(ChainState), st);
+  E.d_bonds = bonds_buf.as<int>();
+  E.d_state = state_buf.as<ChainState>();
+  {
+    std::vector<int> hb((size_t)B * (L + 2));
+    for (int c = 0; c < B; ++c)
+      for (int k = 0; k <= L + 1; ++k) hb[(size_t)c * (L + 2) + k] = k <= L ? q[k] : 1;
+    CK(cudaMemcpyAsync(E.d_bonds, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // hb goes out of scope
+  }
+  CK(init_state(E.d_state, B, st));
+  ++ctx->launches;
+  DevBuf C0((size_t)B * P.ccap * es, st), C1((size_t)B * P.ccap * es, st);
+  DevBuf Rb((size_t)B * P.rcap * es, st), Bb((size_t)B * P.bcap * es, st);
+  DevBuf qrw(P.qr_work ? (size_t)B * P.qr_work * es : 0, st);
+  DevBuf svdw(P.svd_work ? (size_t)B * P.svd_work * es : 0, st);
+  const long long sC = P.ccap, sR = P.rcap, sBb = P.bcap;
+  T* cbuf[2] = {C0.as<T>(), C1.as<T>()};
+  const double tol = s.tolerance;
+
+  // ---- pass 1: exact left-to-right QR (mps.hpp:193-205)
+  int cur = 0;
+  const T* curp = static_cast<const T*>(guess.site[0]);
+  long long s_cur = guess.cap[0];
+  if (L == 1) {
+    CK(cudaMemcpy2DAsync(cbuf[0], sC * es, curp, s_cur * es, (size_t)d[0] * es, B, cudaMemcpyDeviceToDevice, st));
+    curp = cbuf[0];
+    s_cur = sC;
+  }
+  for (int k = 0; k + 1 < L; ++k) {
+    QrParams qp{};
+    qp.A = curp;
+    qp.sA = s_cur;
+    qp.Q = psi->site[k];
+    qp.sQ = P.psi_cap[k];
+    qp.R = Rb.p;
+    qp.sR = sR;
+    qp.work = qrw.p;
+    qp.s_work = P.qr_work;
+    qp.m = q[k] * d[k];
+    qp.n = g[k + 1];
+    CK(householder_qr<T>(qp, B, st));
+    ++ctx->launches;
+    // carried = R * next.right_matrix()  (mps.hpp:202)
+    const int nxt = (k == 0 && curp != cbuf[0]) ? 0 : cur ^ 1;
+    E.G(Rb.p, sR, guess.site[k + 1], guess.cap[k + 1], cbuf[nxt], sC, dconst(q[k + 1]), dconst(d[k + 1] * g[k + 2]),
+        dconst(g[k + 1]), OP_N, OP_N, false);
+    cur = nxt;
+    curp = cbuf[cur];
+    s_cur = sC;
+  }
+  // <T,T>: with the default guess the QR pass is an exact orthogonalisation of
+  // T itself, so |T|^2 = |carried centre|_F^2 (= scprod(T,T), simplify.hpp:37-41)
+  const bool default_guess = (&guess == &target);
+  if (variational) {
+    double* tn2 = reinterpret_cast<double*>(E.d_state) + offsetof(ChainState, target_norm2) / sizeof(double);
+    const long long s_st = sizeof(ChainState) / sizeof(double);
+    if (default_guess) {
+      CK(frob2<T>(curp, s_cur, dconst(q[L - 1] * d[L - 1]), dconst(1), E.d_bonds, E.ld, tn2, s_st, B, st));
+      ++ctx->launches;
+    } else {
+      // env chain <T,T> (mps.hpp:416-423)
+      long long ecap = 1, xcap = 1;
+      for (int k = 0; k < L; ++k) {
+        ecap = std::max(ecap, (long long)t[k] * t[k]);
+        xcap = std::max(xcap, (long long)t[k] * d[k] * t[k + 1]);
+      }
+      DevBuf e0((size_t)B * ecap * es, st), e1((size_t)B * ecap * es, st), xb((size_t)B * xcap * es, st);
+      CK(fill_one<T>(e0.as<T>(), ecap, B, st));
+      ++ctx->launches;
+      T* eb[2] = {e0.as<T>(), e1.as<T>()};
+      for (int k = 0; k < L; ++k) {
+        E.G(eb[k & 1], ecap, target.site[k], target.cap[k], xb.p, xcap, dconst(t[k]), dconst(d[k] * t[k + 1]),
+            dconst(t[k]), OP_N, OP_N, false);
+        E.G(target.site[k], target.cap[k], xb.p, xcap, eb[(k + 1) & 1], ecap, dconst(t[k + 1]), dconst(t[k + 1]),
+            dconst(t[k] * d[k]), OP_C, OP_N, false);
+      }
+      CK(frob2<T>(eb[L & 1], ecap, dconst(1), dconst(1), E.d_bonds, E.ld, tn2, s_st, B, st));  // |<T,T>|
+      ++ctx->launches;
+    }
+  }
+
+  // ---- pass 2: truncating right-to-left sweep (mps.hpp:206-210, 253-265)
+  for (int k = L - 1; k >= 1; --k) {
+    const DimExpr rows = dconst(q[k]);
+    const DimExpr cols = dbond(k + 1, d[k]);
+    E.S(curp, s_cur, rows, cols, k, psi->site[k], P.psi_cap[k], 1, tol, mb, false, true, svdw.p, P.svd_work);
+    // U S = theta V_r  (q_k x r)
+    E.G(curp, s_cur, psi->site[k], P.psi_cap[k], Bb.p, sBb, rows, dbond(k), cols, OP_N, OP_C, false);
+    // prev.left_matrix() * (U S)  (mps.hpp:261)
+    const int nxt = cur ^ 1;
+    E.G(psi->site[k - 1], P.psi_cap[k - 1], Bb.p, sBb, cbuf[nxt], sC, dconst(q[k - 1] * d[k - 1]), dbond(k),
+        dconst(q[k]), OP_N, OP_N, false);
+    cur = nxt;
+    curp = cbuf[cur];
+    s_cur = sC;
+  }
+  // centre tensor at site 0
+  CK(copy_dims<T>(curp, s_cur, static_cast<T*>(psi->site[0]), P.psi_cap[0], dconst(d[0]), dbond(1), E.d_bonds, E.ld,
+                  nullptr, 0, (long long)d[0] * bound[1], B, st));
+  ++ctx->launches;
+  // pass 3: move to the requested centre (mps.hpp:211-213, 238-250)
+  for (int c = 0; c < center; ++c) {
+    CK(copy_dims<T>(static_cast<T*>(psi->site[c]), P.psi_cap[c], cbuf[0], sC, dbond(c, d[c]), dbond(c + 1),
+                    E.d_bonds, E.ld, nullptr, 0, P.psi_cap[c], B, st));
+    ++ctx->launches;
+    CK(copy_bond(E.d_bonds, E.ld, c + 1, L + 1, B, st));  // keep the old bond p_{c+1}
+    ++ctx->launches;
+    E.S(cbuf[0], sC, dbond(c, d[c]), dbond(c + 1), c + 1, psi->site[c], P.psi_cap[c], 0, tol, mb, false, true,
+        svdw.p, P.svd_work);
+    // S V^H = U_r^H theta (r x p_old), then carried into the next site (mps.hpp:246)
+    E.G(psi->site[c], P.psi_cap[c], cbuf[0], sC, Bb.p, sBb, dbond(c + 1), dbond(L + 1), dbond(c, d[c]), OP_C, OP_N,
+        false);
+    E.G(Bb.p, sBb, psi->site[c + 1], P.psi_cap[c + 1], cbuf[1], sC, dbond(c + 1), dbond(c + 2, d[c + 1]),
+        dbond(L + 1), OP_N, OP_N, false);
+    CK(copy_dims<T>(cbuf[1], sC, static_cast<T*>(psi->site[c + 1]), P.psi_cap[c + 1], dbond(c + 1),
+                    dbond(c + 2, d[c + 1]), E.d_bonds, E.ld, nullptr, 0, P.psi_cap[c + 1], B, st));
+    ++ctx->launches;
+  }
+  const int out_center = variational ? 0 : center;
+
+  if (variational && L >= 2) {
+    // ---- environments (simplify.hpp:28-36)
+    std::vector<DevBuf> lenv, renv;
+    lenv.reserve(L + 1);
+    renv.reserve(L + 1);
+    for (int k = 0; k <= L; ++k) {
+      lenv.emplace_back((size_t)B * P.env_cap[k] * es, st);
+      renv.emplace_back((size_t)B * P.env_cap[k] * es, st);
+    }
+    DevBuf XZ((size_t)B * P.xz * es, st), YW((size_t)B * P.yw * es, st), TH((size_t)B * P.th * es, st);
+    const long long sxz = P.xz, syw = P.yw, sth = P.th;
+    CK(fill_one<T>(lenv[0].as<T>(), P.env_cap[0], B, st));
+    CK(fill_one<T>(renv[L].as<T>(), P.env_cap[L], B, st));
+    ctx->launches += 2;
+    auto Ts = [&](int k) { return (const void*)target.site[k]; };
+    auto Tc = [&](int k) { return target.count == 1 ? 0LL : target.cap[k]; };
+    for (int k = L - 1; k >= 1; --k) {
+      // Z = T_k (t_k d x t_{k+1}) . renv[k+1]^T ; renv[k] = conj(psi_k) . Z^T
+      E.G(Ts(k), Tc(k), renv[k + 1].p, P.env_cap[k + 1], XZ.p, sxz, dconst(t[k] * d[k]), dbond(k + 1),
+          dconst(t[k + 1]), OP_N, OP_T, false);
+      E.G(psi->site[k], P.psi_cap[k], XZ.p, sxz, renv[k].p, P.env_cap[k], dbond(k), dconst(t[k]), dbond(k + 1, d[k]),
+          OP_R, OP_T, false);
+    }
+    CK(begin_sweeps(E.d_state, B, st));
+    ++ctx->launches;
+
+    // ---- sweeps (simplify.hpp:66-91, 114-125)
+    const int nsweeps = std::max(1, s.max_sweeps);
+    std::vector<ChainState> hstate(B);
+    for (int sw = 0; sw < nsweeps; ++sw) {
+      for (int n = 0; n + 1 < L; ++n) {  // left to right
+        const int dn = d[n], dn1 = d[n + 1];
+        E.G(lenv[n].p, P.env_cap[n], Ts(n), Tc(n), XZ.p, sxz, dbond(n), dconst(dn * t[n + 1]), dconst(t[n]), OP_N,
+            OP_N, true);
+        E.G(XZ.p, sxz, Ts(n + 1), Tc(n + 1), YW.p, syw, dbond(n, dn), dconst(dn1 * t[n + 2]), dconst(t[n + 1]),
+            OP_N, OP_N, true);
+        E.G(YW.p, syw, renv[n + 2].p, P.env_cap[n + 2], TH.p, sth, dbond(n, dn * dn1), dbond(n + 2),
+            dconst(t[n + 2]), OP_N, OP_T, true);
+        E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n], P.psi_cap[n], 0, tol, mb, true, false,
+            svdw.p, P.svd_work);
+        E.G(psi->site[n], P.psi_cap[n], TH.p, sth, psi->site[n + 1], P.psi_cap[n + 1], dbond(n + 1),
+            dbond(n + 2, dn1), dbond(n, dn), OP_C, OP_N, true);
+        E.G(psi->site[n], P.psi_cap[n], XZ.p, sxz, lenv[n + 1].p, P.env_cap[n + 1], dbond(n + 1),
+            dconst(t[n + 1]), dbond(n, dn), OP_C, OP_N, true);
+      }
+      for (int n = L - 2; n >= 0; --n) {  // right to left
+        const int dn = d[n], dn1 = d[n + 1];
+        E.G(Ts(n + 1), Tc(n + 1), renv[n + 2].p, P.env_cap[n + 2], XZ.p, sxz, dconst(t[n + 1] * dn1), dbond(n + 2),
+            dconst(t[n + 2]), OP_N, OP_T, true);
+        E.G(Ts(n), Tc(n), XZ.p, sxz, YW.p, syw, dconst(t[n] * dn), dbond(n + 2, dn1), dconst(t[n + 1]), OP_N, OP_N,
+            true);
+        E.G(lenv[n].p, P.env_cap[n], YW.p, syw, TH.p, sth, dbond(n), dbond(n + 2, dn * dn1), dconst(t[n]), OP_N,
+            OP_N, true);
+        E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n + 1], P.psi_cap[n + 1], 1, tol, mb, true,
+            false, svdw.p, P.svd_work);
+        E.G(TH.p, sth, psi->site[n + 1], P.psi_cap[n + 1], psi->site[n], P.psi_cap[n], dbond(n, dn), dbond(n + 1),
+            dbond(n + 2, dn1), OP_N, OP_C, true);
+        E.G(psi->site[n + 1], P.psi_cap[n + 1], XZ.p, sxz, renv[n + 1].p, P.env_cap[n + 1], dbond(n + 1),
+            dconst(t[n + 1]), dbond(n + 2, dn1), OP_R, OP_T, true);
+      }
+      CK(sweep_end<T>(static_cast<T*>(psi->site[0]), P.psi_cap[0], dbond(1, d[0]), E.d_bonds, E.ld, E.d_state,
+                      s.simplification_tolerance, sw, B, st));
+      ++ctx->launches;
+      if (sw + 1 < nsweeps) {
+        CK(cudaMemcpyAsync(hstate.data(), E.d_state, B * sizeof(ChainState), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        bool any = false;
+        for (int c = 0; c < B && !any; ++c) any = hstate[c].active != 0;
+        if (!any) break;
+      }
+    }
+  } else if (variational) {
+    // L == 1: the sweep copies the target (simplify.hpp:68-76)
+    CK(cudaMemcpy2DAsync(psi->site[0], P.psi_cap[0] * es, target.site[0], target.cap[0] * es, (size_t)d[0] * es, B,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+
+  // ---- finalize: norms, ledger, zero states, normalisation
+  DevBuf norms((size_t)B * sizeof(double), st);
+  {
+    // centre = out_center; its shape is p_c x d x p_{c+1}
+    std::vector<int> hb((size_t)B * (L + 2));
+    CK(cudaMemcpyAsync(hb.data(), E.d_bonds, hb.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int c = 0; c < B; ++c)
+      for (int k = 0; k <= L; ++k) psi->bonds[(size_t)c * (L + 1) + k] = hb[(size_t)c * (L + 2) + k];
+  }
+  const int cc = out_center;
+  CK(frob2<T>(static_cast<T*>(psi->site[cc]), P.psi_cap[cc], dbond(cc, d[cc]), dbond(cc + 1), E.d_bonds, E.ld,
+              norms.as<double>(), 1, B, st));
+  ++ctx->launches;
+  std::vector<ChainState> hs(B);
+  std::vector<double> hn(B);
+  CK(cudaMemcpyAsync(hs.data(), E.d_state, B * sizeof(ChainState), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hn.data(), norms.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < B; ++c) {
+    if (hs[c].status & ST_NONFINITE) throw Error{TTG_NUMERIC, "schmidt_split: non-finite input"};
+    if (hs[c].status & ST_NOCONV) throw Error{TTG_NUMERIC, "SVD failed to converge"};
+  }
+  std::vector<double> scale(B, 1.0);
+  bool any_scale = false, any_zero = false;
+  std::vector<int> zero(B, 0);
+  for (int c = 0; c < B; ++c) {
+    const double nrm = std::sqrt(std::max(0.0, hn[c]));
+    ttg_report r{};
+    if (variational) {
+      const double tn2 = L == 1 ? hn[c] : hs[c].target_norm2;
+      const double tn = std::sqrt(std::max(0.0, tn2));
+      double residual;
+      int sweeps = hs[c].sweeps;
+      int conv = hs[c].converged;
+      if (L == 1) {
+        residual = fp_error_floor(tn);
+        sweeps = 1;
+        conv = 1;
+      } else if (tn <= fp_error_floor(1.0)) {  // simplify.hpp:107-112
+        residual = tn;
+        conv = 1;
+        zero[c] = 1;
+      } else {
+        residual = std::sqrt(std::max(0.0, hs[c].dist2)) + fp_error_floor(tn);
+      }
+      if (nrm == 0.0) zero[c] = 1;  // simplify.hpp:128-129
+      r.sweeps = sweeps;
+      r.converged = conv;
+      r.residual = residual;
+      r.target_norm2 = tn2;
+      psi->error[c] = target.error[c] + residual;  // simplify.hpp:191
+    } else {
+      // CanonicalMPS ctor ledger (mps.hpp:214-215)
+      psi->error[c] = guess.error[c] + std::sqrt(hs[c].err2) + fp_error_floor(nrm);
+      r.residual = std::sqrt(hs[c].err2);
+      r.target_norm2 = hn[c];
+    }
+    double final_norm = zero[c] ? 0.0 : nrm;
+    if (s.normalize && final_norm > 0.0) {  // mps.hpp:227-235
+      scale[c] = 1.0 / final_norm;
+      any_scale = true;
+      psi->error[c] /= final_norm;
+      final_norm = 1.0;
+    }
+    r.norm = final_norm;
+    r.error = psi->error[c];
+    if (reports) reports[c] = r;
+    any_zero |= zero[c] != 0;
+  }
+  if (any_zero) {
+    for (int c = 0; c < B; ++c) {
+      if (!zero[c]) continue;
+      for (int k = 0; k <= L; ++k) psi->bonds[(size_t)c * (L + 1) + k] = 1;
+      for (int k = 0; k < L; ++k)
+        CK(cudaMemsetAsync(static_cast<char*>(psi->site[k]) + (size_t)c * P.psi_cap[k] * es, 0, (size_t)d[k] * es,
+                           st));
+    }
+  }
+  if (any_scale) {
+    DevBuf f((size_t)B * sizeof(double), st);
+    CK(cudaMemcpyAsync(f.p, scale.data(), B * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(scale_chains<T>(static_cast<T*>(psi->site[cc]), P.psi_cap[cc], P.psi_cap[cc], f.as<double>(), B, st));
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(st));
+  }
+  psi->center = out_center;
+  CK(cudaStreamSynchronize(st));
+  *out = psi_guard.release();
+}
+
+// ---------------------------------------------------------------------------
+// helpers for the ABI
+// ---------------------------------------------------------------------------
+
+ttg_status fail(ttg_ctx* ctx, ttg_status st, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+template <typename F>
+ttg_status guarded(ttg_ctx* ctx, F&& f) {
+  if (!ctx) return TTG_INVALID;
+  try {
+    f();
+    return TTG_OK;
+  } catch (const Error& e) {
+    return fail(ctx, e.st, e.msg);
+  } catch (const std::exception& e) {
+    return fail(ctx, TTG_INVALID, e.what());
+  }
+}
+
+// Convert a batch to complex128 (promotion of real inputs, types.hpp:12-16).
+ttg_dmps* to_complex(ttg_ctx* ctx, const ttg_dmps& m) {
+  std::vector<long long> cap = m.cap;
+  ttg_dmps* o = new_dmps(m.n, TTG_C128, m.count, m.phys, cap, ctx->stream);
+  o->bonds = m.bonds;
+  o->error = m.error;
+  o->center = m.center;
+  for (int k = 0; k < m.n; ++k) {
+    CK(real_to_complex(static_cast<const double*>(m.site[k]), static_cast<cplx*>(o->site[k]),
+                       (long long)m.count * m.cap[k], ctx->stream));
+    ++ctx->launches;
+  }
+  return o;
+}
+
+void check_strategy(const ttg_strategy* s) {
+  if (!s) throw Error{TTG_INVALID, "null strategy"};
+}
+
+void dispatch_simplify(ttg_ctx* ctx, const ttg_dmps* target, const ttg_dmps* guess, const ttg_strategy& s,
+                       bool variational, int center, ttg_dmps** out, ttg_report* reports) {
+  if (!target || !out) throw Error{TTG_INVALID, "null argument"};
+  if (target->n < 1) throw Error{TTG_SHAPE, "empty MPS"};
+  if (!target->uniform()) throw Error{TTG_SHAPE, "batched simplify needs chains of identical shape"};
+  std::unique_ptr<ttg_dmps> promoted_t, promoted_g;
+  const ttg_dmps* T_ = target;
+  const ttg_dmps* G_ = guess ? guess : target;
+  if (guess) {
+    if (guess->n != target->n || guess->count != target->count) throw Error{TTG_SHAPE, "guess/target mismatch"};
+    if (!guess->uniform()) throw Error{TTG_SHAPE, "guess chains must share one shape"};
+    for (int k = 0; k < target->n; ++k)
+      if (guess->phys[k] != target->phys[k]) throw Error{TTG_SHAPE, "guess/target physical dimension mismatch"};
+    if (guess->dtype != target->dtype) {
+      if (target->dtype == TTG_F64) {
+        promoted_t.reset(to_complex(ctx, *target));
+        T_ = promoted_t.get();
+      } else {
+        promoted_g.reset(to_complex(ctx, *guess));
+        G_ = promoted_g.get();
+      }
+    }
+  }
+  if (!guess) G_ = T_;
+  if (T_->dtype == TTG_F64)
+    run_simplify<double>(ctx, *T_, *G_, s, variational, center, out, reports);
+  else
+    run_simplify<cplx>(ctx, *T_, *G_, s, variational, center, out, reports);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* ttg_version(void) { return "ttgpu 0.1 (sm_100a)"; }
+
+ttg_status ttg_create(int device, ttg_ctx** out) {
+  if (!out) return TTG_INVALID;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return TTG_CUDA;
+  }
+  if (device < 0 || device >= n) return TTG_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return TTG_CUDA;
+  auto* c = new ttg_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return TTG_CUDA;
+  }
+  c->stream = c->own;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return TTG_OK;
+}
+
+void ttg_destroy(ttg_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+const char* ttg_last_error(const ttg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+ttg_status ttg_set_stream(ttg_ctx* ctx, void* stream) {
+  if (!ctx) return TTG_INVALID;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return TTG_OK;
+}
+
+ttg_status ttg_synchronize(ttg_ctx* ctx) {
+  return guarded(ctx, [&] { CK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int64_t ttg_kernel_launches(const ttg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!views || !out || count < 1) throw Error{TTG_INVALID, "null argument"};
+    const int n = views[0].n, dtype = views[0].dtype;
+    if (n < 1) throw Error{TTG_SHAPE, "empty MPS"};
+    if (dtype != TTG_F64 && dtype != TTG_C128) throw Error{TTG_INVALID, "unknown dtype"};
+    std::vector<int> phys(n);
+    std::vector<long long> cap(n, 1);
+    for (int k = 0; k < n; ++k) phys[k] = (int)views[0].phys[k];
+    for (int c = 0; c < count; ++c) {
+      const ttg_mps_view& v = views[c];
+      if (v.n != n || v.dtype != dtype) throw Error{TTG_SHAPE, "batch chains differ in length or dtype"};
+      if (v.bonds[0] != 1 || v.bonds[n] != 1) throw Error{TTG_SHAPE, "MPS boundary bonds must have size one"};
+      if (v.error < 0) throw Error{TTG_SHAPE, "MPS error bound must be non-negative"};
+      for (int k = 0; k < n; ++k) {
+        if (v.phys[k] != phys[k]) throw Error{TTG_SHAPE, "batch chains differ in physical dimensions"};
+        if (v.bonds[k] < 1 || v.phys[k] < 1 || v.bonds[k + 1] < 1) throw Error{TTG_SHAPE, "Tensor3 dimensions must be >= 1"};
+        cap[k] = std::max(cap[k], (long long)(v.bonds[k] * v.phys[k] * v.bonds[k + 1]));
+      }
+    }
+    ttg_dmps* m = new_dmps(n, dtype, count, phys, cap, ctx->stream);
+    std::unique_ptr<ttg_dmps> guard(m);
+    const size_t es = esize(dtype);
+    for (int c = 0; c < count; ++c) {
+      const ttg_mps_view& v = views[c];
+      m->error[c] = v.error;
+      for (int k = 0; k <= n; ++k) m->bonds[(size_t)c * (n + 1) + k] = (int)v.bonds[k];
+      for (int k = 0; k < n; ++k) {
+        const size_t bytes = (size_t)(v.bonds[k] * v.phys[k] * v.bonds[k + 1]) * es;
+        CK(cudaMemcpyAsync(static_cast<char*>(m->site[k]) + (size_t)c * cap[k] * es, v.sites[k], bytes,
+                           cudaMemcpyHostToDevice, ctx->stream));
+      }
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = guard.release();
+  });
+}
+
+ttg_status ttg_mps_from_device(ttg_ctx* ctx, int n, int dtype, int count, const int64_t* bonds, const int64_t* phys,
+                               const void* const* dev_sites, const double* errors, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!bonds || !phys || !dev_sites || !out || count < 1 || n < 1) throw Error{TTG_INVALID, "bad argument"};
+    if (bonds[0] != 1 || bonds[n] != 1) throw Error{TTG_SHAPE, "MPS boundary bonds must have size one"};
+    std::vector<int> ph(n);
+    std::vector<long long> cap(n);
+    for (int k = 0; k < n; ++k) {
+      ph[k] = (int)phys[k];
+      cap[k] = bonds[k] * phys[k] * bonds[k + 1];
+    }
+    ttg_dmps* m = new_dmps(n, dtype, count, ph, cap, ctx->stream);
+    std::unique_ptr<ttg_dmps> guard(m);
+    for (int c = 0; c < count; ++c) {
+      for (int k = 0; k <= n; ++k) m->bonds[(size_t)c * (n + 1) + k] = (int)bonds[k];
+      m->error[c] = errors ? errors[c] : 0.0;
+    }
+    for (int k = 0; k < n; ++k)
+      CK(cudaMemcpyAsync(m->site[k], dev_sites[k], (size_t)count * cap[k] * esize(dtype), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+    *out = guard.release();
+  });
+}
+
+void ttg_mps_free(ttg_dmps* m) { delete m; }
+
+ttg_status ttg_mps_info(const ttg_dmps* m, int chain, int* n, int* dtype, int* count, int64_t* bonds, int64_t* phys,
+                        double* error, int* center) {
+  if (!m || chain < 0 || chain >= m->count) return TTG_INVALID;
+  if (n) *n = m->n;
+  if (dtype) *dtype = m->dtype;
+  if (count) *count = m->count;
+  if (bonds)
+    for (int k = 0; k <= m->n; ++k) bonds[k] = m->bond(chain, k);
+  if (phys)
+    for (int k = 0; k < m->n; ++k) phys[k] = m->phys[k];
+  if (error) *error = m->error[chain];
+  if (center) *center = m->center;
+  return TTG_OK;
+}
+
+ttg_status ttg_mps_download(ttg_ctx* ctx, const ttg_dmps* m, int chain, void* const* sites) {
+  return guarded(ctx, [&] {
+    if (!m || !sites || chain < 0 || chain >= m->count) throw Error{TTG_INVALID, "bad argument"};
+    const size_t es = esize(m->dtype);
+    for (int k = 0; k < m->n; ++k) {
+      const size_t bytes = (size_t)m->bond(chain, k) * m->phys[k] * m->bond(chain, k + 1) * es;
+      CK(cudaMemcpyAsync(sites[k], static_cast<const char*>(m->site[k]) + (size_t)chain * m->cap[k] * es, bytes,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+ttg_status ttg_mps_site_ptr(const ttg_dmps* m, int chain, int k, void** ptr, int64_t* elems) {
+  if (!m || chain < 0 || chain >= m->count || k < 0 || k >= m->n) return TTG_INVALID;
+  if (ptr) *ptr = static_cast<char*>(m->site[k]) + (size_t)chain * m->cap[k] * esize(m->dtype);
+  if (elems) *elems = (int64_t)m->bond(chain, k) * m->phys[k] * m->bond(chain, k + 1);
+  return TTG_OK;
+}
+
+ttg_status ttg_mpo_upload(ttg_ctx* ctx, const ttg_mpo_view* v, ttg_dmpo** out) {
+  return guarded(ctx, [&] {
+    if (!v || !out || v->n < 1) throw Error{TTG_INVALID, "bad argument"};
+    if (v->dtype != TTG_F64 && v->dtype != TTG_C128) throw Error{TTG_INVALID, "unknown dtype"};
+    const int n = v->n;
+    if (v->bonds[0] != 1 || v->bonds[n] != 1) throw Error{TTG_SHAPE, "MPO boundary bonds must have size one"};
+    auto* w = new ttg_dmpo();
+    std::unique_ptr<ttg_dmpo> guard(w);
+    w->n = n;
+    w->dtype = v->dtype;
+    w->stream = ctx->stream;
+    for (int k = 0; k <= n; ++k) w->bonds.push_back((int)v->bonds[k]);
+    for (int k = 0; k < n; ++k) {
+      w->dout.push_back((int)v->phys_out[k]);
+      w->din.push_back((int)v->phys_in[k]);
+      const size_t bytes = (size_t)(v->bonds[k] * v->phys_out[k] * v->phys_in[k] * v->bonds[k + 1]) * esize(v->dtype);
+      w->site.push_back(dev_alloc(bytes, ctx->stream));
+      CK(cudaMemcpyAsync(w->site.back(), v->sites[k], bytes, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = guard.release();
+  });
+}
+
+void ttg_mpo_free(ttg_dmpo* w) { delete w; }
+
+ttg_status ttg_apply_raw(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!op || !v || !out) throw Error{TTG_INVALID, "null argument"};
+    if (op->n != v->n) throw Error{TTG_SHAPE, "apply: operator and state sizes differ"};  // mpo.hpp:214-215
+    for (int k = 0; k < v->n; ++k)
+      if (op->din[k] != v->phys[k]) throw Error{TTG_SHAPE, "apply: physical dimension mismatch"};  // mpo.hpp:221-222
+    if (!v->uniform()) throw Error{TTG_SHAPE, "apply on a batch needs chains of identical shape"};
+    const int n = v->n, B = v->count;
+    const int dtype = (op->dtype == TTG_C128 || v->dtype == TTG_C128) ? TTG_C128 : TTG_F64;
+    std::unique_ptr<ttg_dmps> vc;
+    const ttg_dmps* V = v;
+    if (dtype == TTG_C128 && v->dtype == TTG_F64) {
+      vc.reset(to_complex(ctx, *v));
+      V = vc.get();
+    }
+    std::vector<int> phys(n);
+    std::vector<long long> cap(n);
+    for (int k = 0; k < n; ++k) {
+      phys[k] = op->dout[k];
+      cap[k] = (long long)op->bonds[k] * V->bond(0, k) * op->dout[k] * op->bonds[k + 1] * V->bond(0, k + 1);
+    }
+    ttg_dmps* o = new_dmps(n, dtype, B, phys, cap, ctx->stream);
+    std::unique_ptr<ttg_dmps> guard(o);
+    for (int c = 0; c < B; ++c) {
+      for (int k = 0; k <= n; ++k) o->bonds[(size_t)c * (n + 1) + k] = op->bonds[k] * V->bond(0, k);
+      o->error[c] = v->error[c];  // mpo.hpp:237
+    }
+    for (int k = 0; k < n; ++k) {
+      const size_t welems = (size_t)op->bonds[k] * op->dout[k] * op->din[k] * op->bonds[k + 1];
+      if (dtype == TTG_F64) {
+        CK(expand_mpo<double>(static_cast<const double*>(op->site[k]), static_cast<const double*>(V->site[k]),
+                              static_cast<double*>(o->site[k]), op->bonds[k], op->dout[k], op->din[k],
+                              op->bonds[k + 1], V->bond(0, k), V->bond(0, k + 1), B, V->cap[k], cap[k], ctx->stream));
+      } else {
+        DevBuf wc;
+        const cplx* W = static_cast<const cplx*>(op->site[k]);
+        if (op->dtype == TTG_F64) {
+          wc = DevBuf(welems * sizeof(cplx), ctx->stream);
+          CK(real_to_complex(static_cast<const double*>(op->site[k]), wc.as<cplx>(), (long long)welems, ctx->stream));
+          ++ctx->launches;
+          W = wc.as<cplx>();
+        }
+        CK(expand_mpo<cplx>(W, static_cast<const cplx*>(V->site[k]), static_cast<cplx*>(o->site[k]), op->bonds[k],
+                            op->dout[k], op->din[k], op->bonds[k + 1], V->bond(0, k), V->bond(0, k + 1), B, V->cap[k],
+                            cap[k], ctx->stream));
+      }
+      ++ctx->launches;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = guard.release();
+  });
+}
+
+ttg_status ttg_hadamard(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!u || !v || !out) throw Error{TTG_INVALID, "null argument"};
+    if (u->n != v->n) throw Error{TTG_SHAPE, "hadamard: states of different length"};  // blas.hpp:46-47
+    for (int k = 0; k < u->n; ++k)
+      if (u->phys[k] != v->phys[k]) throw Error{TTG_SHAPE, "hadamard: physical dimension mismatch"};  // blas.hpp:53-54
+    if (u->count != v->count) throw Error{TTG_SHAPE, "hadamard: batch sizes differ"};
+    if (!u->uniform() || !v->uniform()) throw Error{TTG_SHAPE, "hadamard on a batch needs identical shapes"};
+    const int n = u->n, B = u->count;
+    const int dtype = (u->dtype == TTG_C128 || v->dtype == TTG_C128) ? TTG_C128 : TTG_F64;
+    std::unique_ptr<ttg_dmps> uc, vc;
+    const ttg_dmps* U = u;
+    const ttg_dmps* V = v;
+    if (dtype == TTG_C128 && u->dtype == TTG_F64) {
+      uc.reset(to_complex(ctx, *u));
+      U = uc.get();
+    }
+    if (dtype == TTG_C128 && v->dtype == TTG_F64) {
+      vc.reset(to_complex(ctx, *v));
+      V = vc.get();
+    }
+    std::vector<long long> cap(n);
+    for (int k = 0; k < n; ++k)
+      cap[k] = (long long)U->bond(0, k) * V->bond(0, k) * u->phys[k] * U->bond(0, k + 1) * V->bond(0, k + 1);
+    ttg_dmps* o = new_dmps(n, dtype, B, u->phys, cap, ctx->stream);
+    std::unique_ptr<ttg_dmps> guard(o);
+    for (int c = 0; c < B; ++c) {
+      for (int k = 0; k <= n; ++k) o->bonds[(size_t)c * (n + 1) + k] = U->bond(0, k) * V->bond(0, k);
+      o->error[c] = u->error[c] + v->error[c];  // blas.hpp:66
+    }
+    for (int k = 0; k < n; ++k) {
+      if (dtype == TTG_F64)
+        CK(expand_hadamard<double>(static_cast<const double*>(U->site[k]), static_cast<const double*>(V->site[k]),
+                                   static_cast<double*>(o->site[k]), U->bond(0, k), u->phys[k], U->bond(0, k + 1),
+                                   V->bond(0, k), V->bond(0, k + 1), B, U->cap[k], V->cap[k], cap[k], ctx->stream));
+      else
+        CK(expand_hadamard<cplx>(static_cast<const cplx*>(U->site[k]), static_cast<const cplx*>(V->site[k]),
+                                 static_cast<cplx*>(o->site[k]), U->bond(0, k), u->phys[k], U->bond(0, k + 1),
+                                 V->bond(0, k), V->bond(0, k + 1), B, U->cap[k], V->cap[k], cap[k], ctx->stream));
+      ++ctx->launches;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = guard.release();
+  });
+}
+
+ttg_status ttg_simplify(ttg_ctx* ctx, const ttg_dmps* target, const ttg_strategy* strategy, const ttg_dmps* guess,
+                        ttg_dmps** out, ttg_report* reports) {
+  return guarded(ctx, [&] {
+    check_strategy(strategy);
+    if (strategy->method == TTG_SVD_TRUNCATE)  // simplify.hpp:184-187
+      dispatch_simplify(ctx, target, nullptr, *strategy, false, 0, out, reports);
+    else
+      dispatch_simplify(ctx, target, guess, *strategy, true, 0, out, reports);
+  });
+}
+
+ttg_status ttg_apply(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, const ttg_strategy* strategy, ttg_dmps** out,
+                     ttg_report* reports) {
+  ttg_dmps* raw = nullptr;
+  ttg_status st = ttg_apply_raw(ctx, op, v, &raw);
+  if (st != TTG_OK) return st;
+  st = ttg_simplify(ctx, raw, strategy, nullptr, out, reports);
+  ttg_mps_free(raw);
+  return st;
+}
+
+ttg_status ttg_canonicalize(ttg_ctx* ctx, const ttg_dmps* v, int center, const ttg_strategy* strategy, ttg_dmps** out,
+                            ttg_report* reports) {
+  return guarded(ctx, [&] {
+    check_strategy(strategy);
+    if (!v) throw Error{TTG_INVALID, "null argument"};
+    if (center < 0 || center >= v->n) throw Error{TTG_SHAPE, "canonical center out of range"};  // mps.hpp:190-191
+    dispatch_simplify(ctx, v, nullptr, *strategy, false, center, out, reports);
+  });
+}
+
+ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double* out_re, double* out_im) {
+  return guarded(ctx, [&] {
+    if (!u || !v || !out_re) throw Error{TTG_INVALID, "null argument"};
+    if (u->n != v->n) throw Error{TTG_SHAPE, "scprod: states of different length"};  // mps.hpp:417-418
+    if (u->count != v->count) throw Error{TTG_SHAPE, "scprod: batch sizes differ"};
+    if (!u->uniform() || !v->uniform()) throw Error{TTG_SHAPE, "scprod on a batch needs identical shapes"};
+    const int dtype = (u->dtype == TTG_C128 || v->dtype == TTG_C128) ? TTG_C128 : TTG_F64;
+    std::unique_ptr<ttg_dmps> uc, vc;
+    const ttg_dmps* U = u;
+    const ttg_dmps* V = v;
+    if (dtype == TTG_C128 && u->dtype == TTG_F64) {
+      uc.reset(to_complex(ctx, *u));
+      U = uc.get();
+    }
+    if (dtype == TTG_C128 && v->dtype == TTG_F64) {
+      vc.reset(to_complex(ctx, *v));
+      V = vc.get();
+    }
+    const int n = u->n, B = u->count;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      Engine<T> E(ctx, n, B);
+      E.ld = n + 1;
+      DevBuf bb((size_t)B * (n + 1) * sizeof(int), ctx->stream);
+      E.d_bonds = bb.as<int>();
+      E.bound.assign(n + 1, 1);
+      long long ecap = 1, xcap = 1;
+      for (int k = 0; k <= n; ++k) ecap = std::max(ecap, (long long)U->bond(0, k) * V->bond(0, k));
+      for (int k = 0; k < n; ++k) xcap = std::max(xcap, (long long)U->bond(0, k) * v->phys[k] * V->bond(0, k + 1));
+      const size_t es = sizeof(T);
+      DevBuf e0((size_t)B * ecap * es, ctx->stream), e1((size_t)B * ecap * es, ctx->stream),
+          xb((size_t)B * xcap * es, ctx->stream);
+      CK(fill_one<T>(e0.as<T>(), ecap, B, ctx->stream));
+      ++ctx->launches;
+      T* eb[2] = {e0.as<T>(), e1.as<T>()};
+      for (int k = 0; k < n; ++k) {
+        const int pu = U->bond(0, k), pv = V->bond(0, k), pu1 = U->bond(0, k + 1), pv1 = V->bond(0, k + 1);
+        const int dk = v->phys[k];
+        E.G(eb[k & 1], ecap, V->site[k], V->cap[k], xb.p, xcap, dconst(pu), dconst(dk * pv1), dconst(pv), OP_N, OP_N,
+            false);
+        E.G(U->site[k], U->cap[k], xb.p, xcap, eb[(k + 1) & 1], ecap, dconst(pu1), dconst(pv1), dconst(pu * dk),
+            OP_C, OP_N, false);
+      }
+      std::vector<T> h((size_t)B * ecap);
+      CK(cudaMemcpyAsync(h.data(), eb[n & 1], h.size() * es, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      for (int c = 0; c < B; ++c) {
+        if constexpr (std::is_same<T, double>::value) {
+          out_re[c] = h[(size_t)c * ecap];
+          if (out_im) out_im[c] = 0.0;
+        } else {
+          out_re[c] = h[(size_t)c * ecap].x;
+          if (out_im) out_im[c] = h[(size_t)c * ecap].y;
+        }
+      }
+    };
+    if (dtype == TTG_F64)
+      run(double{});
+    else
+      run(cplx{});
+  });
+}
+
+}  // extern "C"

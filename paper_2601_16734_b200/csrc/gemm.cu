@@ -1,0 +1,230 @@
+// Batched DMMA GEMM (see gemm.cuh).  Tiles: 64x64x16 per CTA, 4 warps in a
+// 2x2 layout, each warp 32x32 = 2 x 4 m16n8 accumulator tiles.  Operands are
+// staged k-major in shared memory by a 2-stage cp.async pipeline (zero-filled
+// at the ragged edges), rows padded so that the 64-bit (f64) and 128-bit
+// (complex) fragment loads are bank-conflict free.
+#include "gemm.cuh"
+
+namespace ttg {
+namespace {
+
+constexpr int BM = 64, BN = 64, NTHREADS = 128, STAGES = 2;
+
+template <typename T> struct Pad { static constexpr int value = 4; };
+template <> struct Pad<cplx> { static constexpr int value = 2; };
+// k-depth per stage: 16 (f64) / 8 (complex) keeps both stages under 48 KB static smem
+template <typename T> struct Depth { static constexpr int value = 16; };
+template <> struct Depth<cplx> { static constexpr int value = 8; };
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool valid, int bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int src = valid ? bytes : 0;
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+template <typename T, int OPA, int OPB>
+__global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_n) {
+  constexpr int PAD = Pad<T>::value;
+  constexpr int BK = Depth<T>::value;
+  constexpr int KSH = BK == 16 ? 4 : 3;
+  constexpr int SA = BM + PAD, SB = BN + PAD;
+  constexpr bool CPX = Scalar<T>::is_complex;
+  __shared__ __align__(16) T As[STAGES][BK][SA];
+  __shared__ __align__(16) T Bs[STAGES][BK][SB];
+
+  const int chain = blockIdx.y;
+  if (p.st && !p.st[chain].active) return;
+  const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
+  const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
+  const int K = p.K.eval(p.bonds, chain, p.bonds_ld);
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= M || n0 >= N) return;
+
+  const T* A = static_cast<const T*>(p.A) + p.sA * chain;
+  const T* B = static_cast<const T*>(p.B) + p.sB * chain;
+  T* C = static_cast<T*>(p.C) + p.sC * chain;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+
+  double acc[2][4][4];
+  double acci[CPX ? 2 : 1][CPX ? 4 : 1][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+  if constexpr (CPX) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acci[i][j][r] = 0.0;
+  }
+
+  auto load_tile = [&](int stage, int k0) {
+    // A tile: BM x BK, element (m, k) -> As[k][m]
+    if constexpr (OPA == OP_N || OPA == OP_R) {
+      const int kk = tid & (BK - 1), mb = tid >> KSH;
+#pragma unroll
+      for (int i = 0; i < BM * BK / NTHREADS; ++i) {
+        const int m = mb + (NTHREADS / BK) * i;
+        const bool v = (m0 + m < M) && (k0 + kk < K);
+        const T* src = v ? A + (long long)(m0 + m) * K + (k0 + kk) : A;
+        cp_async(&As[stage][kk][m], src, v, sizeof(T));
+      }
+    } else {
+      const int m = tid & 63, kb = tid >> 6;
+#pragma unroll
+      for (int i = 0; i < BK / 2; ++i) {
+        const int kk = kb + 2 * i;
+        const bool v = (m0 + m < M) && (k0 + kk < K);
+        const T* src = v ? A + (long long)(k0 + kk) * M + (m0 + m) : A;
+        cp_async(&As[stage][kk][m], src, v, sizeof(T));
+      }
+    }
+    // B tile: BK x BN, element (k, n) -> Bs[k][n]
+    if constexpr (OPB == OP_N || OPB == OP_R) {
+      const int n = tid & 63, kb = tid >> 6;
+#pragma unroll
+      for (int i = 0; i < BK / 2; ++i) {
+        const int kk = kb + 2 * i;
+        const bool v = (n0 + n < N) && (k0 + kk < K);
+        const T* src = v ? B + (long long)(k0 + kk) * N + (n0 + n) : B;
+        cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
+      }
+    } else {
+      const int kk = tid & (BK - 1), nb = tid >> KSH;
+#pragma unroll
+      for (int i = 0; i < BN * BK / NTHREADS; ++i) {
+        const int n = nb + (NTHREADS / BK) * i;
+        const bool v = (n0 + n < N) && (k0 + kk < K);
+        const T* src = v ? B + (long long)(n0 + n) * K + (k0 + kk) : B;
+        cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
+      }
+    }
+  };
+
+  const int ktiles = (K + BK - 1) / BK;
+  if (ktiles > 0) load_tile(0, 0);
+  cp_commit();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int stage = kt & 1;
+    if (kt + 1 < ktiles) load_tile(stage ^ 1, (kt + 1) * BK);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if constexpr (!CPX) {
+        double a[2][2], b[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          a[i][0] = As[stage][kk + t4][wm + i * 16 + g];
+          a[i][1] = As[stage][kk + t4][wm + i * 16 + g + 8];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[stage][kk + t4][wn + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i][0], a[i][1], b[j]);
+      } else {
+        constexpr double sa = (OPA == OP_C || OPA == OP_R) ? -1.0 : 1.0;
+        constexpr double sb = (OPB == OP_C || OPB == OP_R) ? -1.0 : 1.0;
+        double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const cplx x0 = As[stage][kk + t4][wm + i * 16 + g];
+          const cplx x1 = As[stage][kk + t4][wm + i * 16 + g + 8];
+          ar[i][0] = x0.x; ai[i][0] = sa * x0.y; nai[i][0] = -ai[i][0];
+          ar[i][1] = x1.x; ai[i][1] = sa * x1.y; nai[i][1] = -ai[i][1];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const cplx y = Bs[stage][kk + t4][wn + j * 8 + g];
+          br[j] = y.x; bi[j] = sb * y.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma(acc[i][j], ar[i][0], ar[i][1], br[j]);
+            dmma(acc[i][j], nai[i][0], nai[i][1], bi[j]);
+            dmma(acci[i][j], ar[i][0], ar[i][1], bi[j]);
+            dmma(acci[i][j], ai[i][0], ai[i][1], br[j]);
+          }
+      }
+    }
+    __syncthreads();
+  }
+
+  // epilogue: c0,c1 -> (g, 2t..2t+1), c2,c3 -> (g+8, 2t..2t+1)
+  const double alpha = p.alpha;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + wm + i * 16 + g + (r >= 2 ? 8 : 0);
+        const int n = n0 + wn + j * 8 + 2 * t4 + (r & 1);
+        if (m < M && n < N) {
+          T* dst = C + (long long)m * N + n;
+          if constexpr (!CPX) {
+            const double v = alpha * acc[i][j][r];
+            *dst = p.beta ? *dst + v : v;
+          } else {
+            cplx v{alpha * acc[i][j][r], alpha * acci[i][j][r]};
+            if (p.beta) v = add(*dst, v);
+            *dst = v;
+          }
+        }
+      }
+}
+
+template <typename T, int OPA>
+cudaError_t launch_b(const GemmParams& p, int opB, dim3 grid, int tiles_n, cudaStream_t s) {
+  switch (opB) {
+    case OP_N: gemm_kernel<T, OPA, OP_N><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
+    case OP_T: gemm_kernel<T, OPA, OP_T><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
+    case OP_C: gemm_kernel<T, OPA, OP_C><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
+    default: gemm_kernel<T, OPA, OP_R><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int chains, cudaStream_t s) {
+  if (mmax <= 0 || nmax <= 0 || chains <= 0) return cudaSuccess;
+  const int tiles_m = (mmax + BM - 1) / BM, tiles_n = (nmax + BN - 1) / BN;
+  dim3 grid(tiles_m * tiles_n, chains);
+  switch (opA) {
+    case OP_N: return launch_b<T, OP_N>(p, opB, grid, tiles_n, s);
+    case OP_T: return launch_b<T, OP_T>(p, opB, grid, tiles_n, s);
+    case OP_C: return launch_b<T, OP_C>(p, opB, grid, tiles_n, s);
+    default: return launch_b<T, OP_R>(p, opB, grid, tiles_n, s);
+  }
+}
+
+template cudaError_t gemm<double>(const GemmParams&, int, int, int, int, int, cudaStream_t);
+template cudaError_t gemm<cplx>(const GemmParams&, int, int, int, int, int, cudaStream_t);
+
+}  // namespace ttg

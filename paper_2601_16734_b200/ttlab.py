@@ -1,0 +1,378 @@
+"""Python mirror of the reference's hot-path API, executed on the B200.
+
+Names, argument meaning and error behaviour follow `ttlab`
+(/root/reference/proj/include/ttlab/): `Strategy` (types.hpp:50-94),
+`apply` (blas.hpp:8-11), `hadamard` (blas.hpp:45-67), `simplify`
+(simplify.hpp:182-195), `canonicalize` (mps.hpp:310-313), `scprod`
+(mps.hpp:416-423), `detail::apply_raw` (mpo.hpp:213-238).  Every operation
+runs through the C ABI of `libttgpu.so`; there is no CPU path.
+
+States are `DeviceMPS` handles (device resident, optionally a batch of
+identically shaped chains).  Host tensors are lists of numpy arrays shaped
+(left, phys, right) for an MPS and (left, out, in, right) for an MPO.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, replace
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib
+
+UNBOUNDED_BOND = (1 << 63) - 1
+SVD_TRUNCATE, VARIATIONAL = 0, 1
+
+
+class ShapeError(ValueError):
+    """shape_error (types.hpp:22-25)."""
+
+
+class CapacityError(RuntimeError):
+    """capacity_error (types.hpp:28-31)."""
+
+
+class NumericError(RuntimeError):
+    """numeric_error (types.hpp:34-37)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no B200 visible."""
+
+
+@dataclass(frozen=True)
+class Strategy:
+    """types.hpp:50-88."""
+
+    method: int = VARIATIONAL
+    tolerance: float = 1e-12
+    simplification_tolerance: float = 1e-12
+    max_bond: int = UNBOUNDED_BOND
+    max_sweeps: int = 4
+    normalize: bool = False
+
+    def with_method(self, m):
+        return replace(self, method=m)
+
+    def with_tolerance(self, t):
+        return replace(self, tolerance=t)
+
+    def with_simplification_tolerance(self, t):
+        return replace(self, simplification_tolerance=t)
+
+    def with_max_bond(self, chi):
+        return replace(self, max_bond=chi)
+
+    def with_max_sweeps(self, s):
+        return replace(self, max_sweeps=s)
+
+    def with_normalize(self, f):
+        return replace(self, normalize=f)
+
+    def _c(self) -> _lib.ttg_strategy:
+        mb = self.max_bond if self.max_bond < (1 << 31) - 1 else 0
+        return _lib.ttg_strategy(int(self.method), float(self.tolerance), float(self.simplification_tolerance),
+                                 int(mb), int(self.max_sweeps), int(bool(self.normalize)))
+
+
+DEFAULT_STRATEGY = Strategy()
+NO_TRUNCATION = Strategy(SVD_TRUNCATE, 0.0, 0.0, UNBOUNDED_BOND, 4, False)
+
+_ERRORS = {
+    _lib.TTG_SHAPE: ShapeError,
+    _lib.TTG_CAPACITY: CapacityError,
+    _lib.TTG_NUMERIC: NumericError,
+    _lib.TTG_CUDA: DeviceError,
+    _lib.TTG_INVALID: ValueError,
+}
+
+
+class Context:
+    """One ttg_ctx (CUDA stream + launch counter) per host thread and device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = lib.ttg_create(int(device), C.byref(h))
+        if st != _lib.TTG_OK:
+            raise DeviceError(f"ttg_create(device={device}) failed with status {st}: no usable CUDA device")
+        self.handle = h
+        self.device = device
+
+    def check(self, status: int):
+        if status != _lib.TTG_OK:
+            msg = lib.ttg_last_error(self.handle).decode()
+            raise _ERRORS.get(status, RuntimeError)(msg)
+
+    def set_stream(self, stream_ptr: int):
+        self.check(lib.ttg_set_stream(self.handle, C.c_void_p(stream_ptr)))
+
+    def synchronize(self):
+        self.check(lib.ttg_synchronize(self.handle))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib.ttg_kernel_launches(self.handle))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.ttg_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def context(device: int = 0) -> Context:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+def _dtype_code(arrs) -> int:
+    return _lib.TTG_C128 if any(np.iscomplexobj(a) for a in arrs) else _lib.TTG_F64
+
+
+def _np_dtype(code):
+    return np.complex128 if code == _lib.TTG_C128 else np.float64
+
+
+def _i64(vals):
+    return (C.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+class DeviceMPS:
+    """Device-resident MPS batch (`ttg_dmps`): `count` chains of one length."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+
+    # ---- construction
+    @classmethod
+    def from_tensors(cls, tensors: Sequence[np.ndarray], error: float = 0.0, ctx: Optional[Context] = None):
+        return cls.from_batch([tensors], [error], ctx)
+
+    @classmethod
+    def from_batch(cls, chains: Sequence[Sequence[np.ndarray]], errors=None, ctx: Optional[Context] = None):
+        ctx = ctx or context()
+        code = _dtype_code([t for ch in chains for t in ch])
+        dt = _np_dtype(code)
+        views = (_lib.ttg_mps_view * len(chains))()
+        keep = []
+        for i, ch in enumerate(chains):
+            arrs = [np.ascontiguousarray(t, dtype=dt) for t in ch]
+            for a in arrs:
+                if a.ndim != 3:
+                    raise ShapeError("MPS tensors must be rank 3 (left, phys, right)")
+            for a, b in zip(arrs[:-1], arrs[1:]):
+                if a.shape[2] != b.shape[0]:
+                    raise ShapeError("MPS bond mismatch between neighboring tensors")
+            bonds = _i64([arrs[0].shape[0]] + [a.shape[2] for a in arrs])
+            phys = _i64([a.shape[1] for a in arrs])
+            ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+            keep += [arrs, bonds, phys, ptrs]
+            err = 0.0 if errors is None else float(errors[i])
+            views[i] = _lib.ttg_mps_view(len(arrs), code, bonds, phys, ptrs, err)
+        h = C.c_void_p()
+        ctx.check(lib.ttg_mps_upload(ctx.handle, views, len(chains), C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_device(cls, n, dtype_code, count, bonds, phys, dev_ptrs, errors=None, ctx: Optional[Context] = None):
+        """Copy device-resident packed site buffers (e.g. torch tensors' data_ptr)."""
+        ctx = ctx or context()
+        h = C.c_void_p()
+        errs = None if errors is None else (C.c_double * count)(*errors)
+        ptrs = (C.c_void_p * n)(*dev_ptrs)
+        ctx.check(lib.ttg_mps_from_device(ctx.handle, n, dtype_code, count, _i64(bonds), _i64(phys), ptrs, errs,
+                                          C.byref(h)))
+        return cls(h, ctx)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.ttg_mps_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    # ---- shape / readback
+    def info(self, chain: int = 0):
+        n, dt, cnt, ctr = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        err = C.c_double()
+        st = lib.ttg_mps_info(self.handle, chain, C.byref(n), C.byref(dt), C.byref(cnt), None, None, None, None)
+        if st != _lib.TTG_OK:
+            raise ValueError("bad chain index")
+        bonds = (C.c_int64 * (n.value + 1))()
+        phys = (C.c_int64 * n.value)()
+        lib.ttg_mps_info(self.handle, chain, None, None, None, bonds, phys, C.byref(err), C.byref(ctr))
+        return dict(n=n.value, dtype=dt.value, count=cnt.value, bonds=list(bonds), phys=list(phys),
+                    error=err.value, center=ctr.value)
+
+    def __len__(self):
+        return self.info()["n"]
+
+    @property
+    def count(self) -> int:
+        return self.info()["count"]
+
+    def bond_dimensions(self, chain: int = 0) -> List[int]:
+        return self.info(chain)["bonds"]
+
+    def max_bond_dimension(self, chain: int = 0) -> int:
+        return max(self.bond_dimensions(chain))
+
+    def error(self, chain: int = 0) -> float:
+        return self.info(chain)["error"]
+
+    @property
+    def center(self) -> int:
+        return self.info()["center"]
+
+    def to_tensors(self, chain: int = 0) -> List[np.ndarray]:
+        inf = self.info(chain)
+        dt = _np_dtype(inf["dtype"])
+        b, p = inf["bonds"], inf["phys"]
+        arrs = [np.empty((b[k], p[k], b[k + 1]), dtype=dt) for k in range(inf["n"])]
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        self.ctx.check(lib.ttg_mps_download(self.ctx.handle, self.handle, chain, ptrs))
+        return arrs
+
+    def site_ptr(self, chain: int, k: int):
+        ptr, n = C.c_void_p(), C.c_int64()
+        if lib.ttg_mps_site_ptr(self.handle, chain, k, C.byref(ptr), C.byref(n)) != _lib.TTG_OK:
+            raise ValueError("bad site")
+        return ptr.value, n.value
+
+
+class DeviceMPO:
+    """Device-resident MPO (`ttg_dmpo`)."""
+
+    def __init__(self, tensors: Sequence[np.ndarray], ctx: Optional[Context] = None):
+        ctx = ctx or context()
+        code = _dtype_code(tensors)
+        arrs = [np.ascontiguousarray(t, dtype=_np_dtype(code)) for t in tensors]
+        for a in arrs:
+            if a.ndim != 4:
+                raise ShapeError("MPO tensors must be rank 4 (left, out, in, right)")
+        for a, b in zip(arrs[:-1], arrs[1:]):
+            if a.shape[3] != b.shape[0]:
+                raise ShapeError("MPO bond mismatch between neighboring tensors")
+        bonds = _i64([arrs[0].shape[0]] + [a.shape[3] for a in arrs])
+        view = _lib.ttg_mpo_view(len(arrs), code, bonds, _i64([a.shape[1] for a in arrs]),
+                                 _i64([a.shape[2] for a in arrs]),
+                                 (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs]))
+        h = C.c_void_p()
+        ctx.check(lib.ttg_mpo_upload(ctx.handle, C.byref(view), C.byref(h)))
+        self.handle, self.ctx = h, ctx
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.ttg_mpo_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def _as_mps(v, ctx=None) -> DeviceMPS:
+    if isinstance(v, DeviceMPS):
+        return v
+    return DeviceMPS.from_tensors(list(v), ctx=ctx)
+
+
+def _as_mpo(op, ctx=None) -> DeviceMPO:
+    if isinstance(op, DeviceMPO):
+        return op
+    return DeviceMPO(list(op), ctx=ctx)
+
+
+def _reports(n):
+    return (_lib.ttg_report * n)()
+
+
+def _report_dicts(reps, n):
+    return [dict(sweeps=r.sweeps, converged=bool(r.converged), residual=r.residual, error=r.error, norm=r.norm,
+                 target_norm2=r.target_norm2) for r in reps[:n]]
+
+
+def apply_raw(op, v) -> DeviceMPS:
+    """mpo.hpp:213-238."""
+    v = _as_mps(v)
+    op = _as_mpo(op, v.ctx)
+    h = C.c_void_p()
+    v.ctx.check(lib.ttg_apply_raw(v.ctx.handle, op.handle, v.handle, C.byref(h)))
+    return DeviceMPS(h, v.ctx)
+
+
+def hadamard(u, v) -> DeviceMPS:
+    """blas.hpp:45-67."""
+    u = _as_mps(u)
+    v = _as_mps(v, u.ctx)
+    h = C.c_void_p()
+    u.ctx.check(lib.ttg_hadamard(u.ctx.handle, u.handle, v.handle, C.byref(h)))
+    return DeviceMPS(h, u.ctx)
+
+
+def simplify(target, strategy: Strategy = DEFAULT_STRATEGY, guess=None, report: Optional[list] = None) -> DeviceMPS:
+    """simplify.hpp:182-195 (also the batched simplify when `target` is a batch)."""
+    t = _as_mps(target)
+    g = None if guess is None else _as_mps(guess, t.ctx)
+    cnt = t.count
+    reps = _reports(cnt)
+    h = C.c_void_p()
+    t.ctx.check(lib.ttg_simplify(t.ctx.handle, t.handle, C.byref(strategy._c()), None if g is None else g.handle,
+                                 C.byref(h), reps))
+    if report is not None:
+        report.extend(_report_dicts(reps, cnt))
+    return DeviceMPS(h, t.ctx)
+
+
+def apply(op, v, strategy: Strategy = DEFAULT_STRATEGY, report: Optional[list] = None) -> DeviceMPS:
+    """blas.hpp:8-11."""
+    v = _as_mps(v)
+    op = _as_mpo(op, v.ctx)
+    cnt = v.count
+    reps = _reports(cnt)
+    h = C.c_void_p()
+    v.ctx.check(lib.ttg_apply(v.ctx.handle, op.handle, v.handle, C.byref(strategy._c()), C.byref(h), reps))
+    if report is not None:
+        report.extend(_report_dicts(reps, cnt))
+    return DeviceMPS(h, v.ctx)
+
+
+def canonicalize(v, center: int = 0, strategy: Strategy = DEFAULT_STRATEGY,
+                 report: Optional[list] = None) -> DeviceMPS:
+    """mps.hpp:310-313."""
+    v = _as_mps(v)
+    cnt = v.count
+    reps = _reports(cnt)
+    h = C.c_void_p()
+    v.ctx.check(lib.ttg_canonicalize(v.ctx.handle, v.handle, int(center), C.byref(strategy._c()), C.byref(h), reps))
+    if report is not None:
+        report.extend(_report_dicts(reps, cnt))
+    return DeviceMPS(h, v.ctx)
+
+
+def scprod(u, v) -> np.ndarray:
+    """mps.hpp:416-423, one value per chain."""
+    u = _as_mps(u)
+    v = _as_mps(v, u.ctx)
+    cnt = u.count
+    re, im = (C.c_double * cnt)(), (C.c_double * cnt)()
+    u.ctx.check(lib.ttg_scprod(u.ctx.handle, u.handle, v.handle, re, im))
+    out = np.array(re[:]) + 1j * np.array(im[:])
+    return out
+
+
+def norm(v) -> np.ndarray:
+    """MPS::norm (mps.hpp:86) per chain."""
+    return np.sqrt(np.maximum(0.0, scprod(v, v).real))

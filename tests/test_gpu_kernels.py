@@ -1,0 +1,156 @@
+"""Kernel-level parity: DMMA GEMM, Householder QR and the truncated Jacobi SVD
+against numpy, through the C-ABI test hooks of libttgpu.so."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+OPS = {0: lambda x: x, 1: lambda x: x.T, 2: lambda x: x.conj().T, 3: lambda x: x.conj()}
+
+
+def _lib():
+    from paper_2601_16734_b200._lib import lib
+    return lib
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _gemm(opA, opB, A, B, M, N, K, batch):
+    lib = _lib()
+    cplx = np.iscomplexobj(A)
+    Cm = np.empty((batch, M, N), dtype=A.dtype)
+    st = lib.ttg_debug_gemm(1 if cplx else 0, opA, opB, M, N, K, batch, _ptr(A), _ptr(B), _ptr(Cm))
+    assert st == 0
+    return Cm
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+@pytest.mark.parametrize("opA", [0, 1, 2, 3])
+@pytest.mark.parametrize("opB", [0, 1, 2, 3])
+def test_gemm_ops(dtype, opA, opB):
+    rng = np.random.default_rng(opA * 4 + opB)
+    for (M, N, K) in [(1, 1, 1), (5, 7, 3), (64, 64, 16), (65, 130, 17), (128, 96, 200), (3, 190, 1)]:
+        batch = 2
+
+        def rnd(*s):
+            x = rng.standard_normal(s)
+            if dtype == np.complex128:
+                x = x + 1j * rng.standard_normal(s)
+            return x
+
+        Ash = (batch, M, K) if opA in (0, 3) else (batch, K, M)
+        Bsh = (batch, K, N) if opB in (0, 3) else (batch, N, K)
+        A, B = np.ascontiguousarray(rnd(*Ash)), np.ascontiguousarray(rnd(*Bsh))
+        got = _gemm(opA, opB, A, B, M, N, K, batch)
+        for b in range(batch):
+            ref = OPS[opA](A[b]) @ OPS[opB](B[b])
+            err = np.abs(got[b] - ref).max() / max(1.0, np.abs(ref).max())
+            assert err < 1e-13, (M, N, K, err)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 3), (8, 4), (4, 8), (64, 32), (130, 70), (384, 192), (96, 200)])
+def test_householder_qr(dtype, shape):
+    lib = _lib()
+    m, n = shape
+    k = min(m, n)
+    rng = np.random.default_rng(m * 1000 + n)
+    A = rng.standard_normal((m, n))
+    if dtype == np.complex128:
+        A = A + 1j * rng.standard_normal((m, n))
+    A = np.ascontiguousarray(A)
+    Q = np.empty((m, k), dtype=dtype)
+    R = np.empty((k, n), dtype=dtype)
+    assert lib.ttg_debug_qr(1 if dtype == np.complex128 else 0, m, n, _ptr(A), _ptr(Q), _ptr(R)) == 0
+    assert np.abs(Q.conj().T @ Q - np.eye(k)).max() < 1e-13
+    assert np.abs(Q @ R - A).max() < 1e-12 * max(1, np.abs(A).max())
+    assert np.abs(np.tril(R, -1)).max() == 0.0
+
+
+def test_qr_rank_deficient():
+    lib = _lib()
+    rng = np.random.default_rng(5)
+    A = np.ascontiguousarray(rng.standard_normal((40, 3)) @ rng.standard_normal((3, 20)))
+    Q, R = np.empty((20, 20))[:0], None
+    Q = np.empty((40, 20))
+    R = np.empty((20, 20))
+    assert lib.ttg_debug_qr(0, 40, 20, _ptr(A), _ptr(Q), _ptr(R)) == 0
+    assert np.abs(Q.T @ Q - np.eye(20)).max() < 1e-13
+    assert np.abs(Q @ R - A).max() < 1e-12 * np.abs(A).max()
+
+
+def _svd(theta, mode, tol=0.0, max_bond=0):
+    lib = _lib()
+    m, n = theta.shape
+    cplx = np.iscomplexobj(theta)
+    theta = np.ascontiguousarray(theta)
+    iso = np.empty(max(m, n) * max(m, n), dtype=theta.dtype)
+    sv = np.empty(min(m, n))
+    r, e2 = C.c_int(), C.c_double()
+    st = lib.ttg_debug_svd(1 if cplx else 0, m, n, _ptr(theta), mode, tol, max_bond, _ptr(iso),
+                           sv.ctypes.data_as(C.POINTER(C.c_double)), C.byref(r), C.byref(e2))
+    assert st == 0
+    r = r.value
+    iso = iso[:m * r].reshape(m, r) if mode == 0 else iso[:r * n].reshape(r, n)
+    return iso, sv, r, e2.value
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (4, 4), (6, 4), (4, 6), (32, 32), (128, 128), (64, 150), (192, 128)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_jacobi_svd_random(dtype, shape, mode):
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    th = rng.standard_normal((m, n))
+    if dtype == np.complex128:
+        th = th + 1j * rng.standard_normal((m, n))
+    iso, sv, r, e2 = _svd(th, mode)
+    ref = np.linalg.svd(th, compute_uv=False)
+    assert np.abs(sv - ref).max() <= 1e-13 * ref[0]
+    assert r == min(m, n)
+    if mode == 0:
+        assert np.abs(iso.conj().T @ iso - np.eye(r)).max() < 1e-12
+        # U_r U_r^H theta == theta (full rank kept)
+        assert np.abs(iso @ (iso.conj().T @ th) - th).max() < 1e-12 * ref[0]
+    else:
+        assert np.abs(iso @ iso.conj().T - np.eye(r)).max() < 1e-12
+        assert np.abs((th @ iso.conj().T) @ iso - th).max() < 1e-12 * ref[0]
+
+
+def test_svd_kat_identity():
+    """test_core.cpp:74-90: theta = I/sqrt(2)."""
+    th = np.eye(2) / np.sqrt(2.0)
+    iso, sv, r, e2 = _svd(th, 0)
+    assert r == 2 and e2 == 0.0
+    assert np.allclose(sv, [1 / np.sqrt(2)] * 2, rtol=0, atol=1e-15)
+    iso, sv, r, e2 = _svd(th, 0, max_bond=1)
+    assert r == 1 and abs(np.sqrt(e2) - 1 / np.sqrt(2)) < 1e-15
+
+
+def test_svd_truncation_rule():
+    """schmidt.hpp:40-59: strict > tol*s0, at least 1, at most max_bond; err = sqrt(sum dropped^2)."""
+    rng = np.random.default_rng(3)
+    U, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    V, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    s = np.array([1.0, 0.5, 0.25, 1e-3, 1e-6, 1e-9, 1e-11, 1e-13, 1e-15, 0.0])
+    th = (U * s) @ V.T
+    _, sv, r, e2 = _svd(th, 0, tol=1e-10)
+    assert r == 6
+    assert abs(np.sqrt(e2) - np.sqrt(np.sum(s[6:] ** 2))) < 1e-15
+    _, sv, r, e2 = _svd(th, 1, tol=1e-10, max_bond=3)
+    assert r == 3
+    assert abs(np.sqrt(e2) - np.sqrt(np.sum(s[3:] ** 2))) < 1e-15
+    _, _, r, _ = _svd(np.zeros((3, 3)), 0, tol=1e-10)
+    assert r == 1
+
+
+def test_svd_rank_deficient_drops_zero_values():
+    rng = np.random.default_rng(11)
+    th = rng.standard_normal((64, 5)) @ rng.standard_normal((5, 64))
+    _, sv, r, _ = _svd(th, 0, tol=1e-12)
+    assert r == 5
+    assert sv[5] < 1e-12 * sv[0]

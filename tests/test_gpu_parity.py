@@ -1,0 +1,268 @@
+"""Engine parity against the oracle on gauge-invariant quantities."""
+import numpy as np
+import pytest
+
+from oracle import ttlab_oracle as O
+from paper_2601_16734_b200 import inputs as I
+
+from ._compare import dense, distance, rel, spectra
+
+pytestmark = pytest.mark.gpu
+
+
+def T():
+    from paper_2601_16734_b200 import ttlab
+    return ttlab
+
+
+def omps(tensors, err=0.0):
+    return O.MPS([np.asarray(t) for t in tensors], err)
+
+
+# ---------------------------------------------------------------- expansions
+def test_apply_raw_identity_and_random():
+    """test_core.cpp:200-227."""
+    t = T()
+    v = O.random_uniform_mps(5, 2, 3, 21)
+    out = t.apply_raw(O.mpo_identity(5, 2).tensors, v.tensors)
+    assert np.abs(dense(out.to_tensors()) - O.mps_to_dense(v)).max() < 1e-14
+    state = O.random_uniform_mps(4, 2, 3, 31)
+    from oracle.rng import random_matrix
+    a = O.mpo_from_local_operators([random_matrix(2, 2, s) for s in (1, 2, 3, 4)])
+    b = O.mpo_from_local_operators([random_matrix(2, 2, s) for s in (5, 6, 7, 8)])
+    s = O.mpo_sum([0.5 + 0.25j, -1 + 1j], [a, b])
+    got = t.apply_raw(s.tensors, state.tensors)
+    ref = O.apply_raw(s, state)
+    for x, y in zip(got.to_tensors(), ref.tensors):
+        assert x.shape == y.shape
+        assert np.abs(x - y).max() <= 1e-14 * np.abs(y).max()
+    assert np.abs(dense(got.to_tensors()) - O.mpo_to_dense(s) @ O.mps_to_dense(state)).max() < 1e-12
+
+
+def test_apply_raw_laplacian_elementwise():
+    t = T()
+    psi = I.random_mps(12, 2, 16, 7)
+    W = I.laplacian_mpo(12)
+    got = t.apply_raw(W, psi).to_tensors()
+    ref = O.apply_raw(O.MPO(W), omps(psi)).tensors
+    for x, y in zip(got, ref):
+        assert x.shape == y.shape and x.dtype == np.float64
+        assert np.abs(x - y).max() <= 1e-14 * max(np.abs(y).max(), 1e-300)
+
+
+def test_apply_shape_errors():
+    """test_blas.cpp:126-129."""
+    t = T()
+    with pytest.raises(t.ShapeError):
+        t.apply(O.mpo_identity(3, 2).tensors, O.random_uniform_mps(4, 2, 1, 1).tensors)
+    with pytest.raises(t.ShapeError):
+        t.apply(O.mpo_identity(4, 3).tensors, O.random_uniform_mps(4, 2, 1, 1).tensors)
+
+
+def test_hadamard_parity():
+    """test_blas.cpp:181-202: dense oracle and exact bond product."""
+    t = T()
+    u = O.random_uniform_mps(5, 2, 2, 20)
+    v = O.random_uniform_mps(5, 2, 3, 21)
+    w = t.hadamard(u.tensors, v.tensors)
+    assert w.bond_dimensions() == [a * b for a, b in zip(u.bond_dimensions(), v.bond_dimensions())]
+    assert np.abs(dense(w.to_tensors()) - O.mps_to_dense(u) * O.mps_to_dense(v)).max() < 1e-12
+    ones = O.product_state(4, np.ones(2))
+    x = O.random_uniform_mps(4, 2, 3, 19)
+    assert np.abs(dense(t.hadamard(x.tensors, ones.tensors).to_tensors()) - O.mps_to_dense(x)).max() < 1e-13
+    e1, e2 = O.basis_state(3, 2, 1), O.basis_state(3, 2, 2)
+    assert np.linalg.norm(dense(t.hadamard(e1.tensors, e2.tensors).to_tensors())) == 0.0
+    # elementwise against the oracle, complex
+    a = I.random_mps(8, 2, 6, 3, complex_=True)
+    b = I.random_mps(8, 2, 5, 4, complex_=True)
+    got = t.hadamard(a, b).to_tensors()
+    ref = O.hadamard(omps(a), omps(b)).tensors
+    for x, y in zip(got, ref):
+        assert np.abs(x - y).max() <= 1e-15 * np.abs(y).max() * 4
+    with pytest.raises(t.ShapeError):
+        t.hadamard(O.random_uniform_mps(3, 2, 2, 1).tensors, O.random_uniform_mps(4, 2, 2, 1).tensors)
+
+
+# ---------------------------------------------------------------- canonical form
+def _isometries(tensors, center):
+    for n, A in enumerate(tensors):
+        if n < center:
+            a = A.reshape(-1, A.shape[2])
+            assert np.abs(a.conj().T @ a - np.eye(a.shape[1])).max() <= 1e-12
+        elif n > center:
+            b = A.reshape(A.shape[0], -1)
+            assert np.abs(b @ b.conj().T - np.eye(b.shape[0])).max() <= 1e-12
+
+
+def test_canonicalize_pins():
+    """test_core.cpp:119-155."""
+    t = T()
+    state = O.random_uniform_mps(6, 2, 5, 42)
+    for center in (0, 2, 5):
+        c = t.canonicalize(state.tensors, center, t.NO_TRUNCATION)
+        assert c.center == center
+        ts = c.to_tensors()
+        _isometries(ts, center)
+        assert np.abs(dense(ts) - O.mps_to_dense(state)).max() < 1e-12
+    state = O.random_uniform_mps(8, 2, 8, 3)
+    exact = O.mps_to_dense(state)
+    c = t.canonicalize(state.tensors, 3, t.NO_TRUNCATION.with_max_bond(4))
+    ts = c.to_tensors()
+    dist = np.linalg.norm(dense(ts) - exact)
+    assert dist <= c.error()
+    assert abs(dist - c.error()) < 1e-10 * np.linalg.norm(exact)
+    assert max(c.bond_dimensions()) <= 4
+    _isometries(ts, 3)
+    ref = O.canonicalize(state, 3, O.NO_TRUNCATION.with_max_bond(4))
+    assert c.bond_dimensions() == ref.bond_dimensions()
+    assert abs(c.error() - ref.error) < 1e-12
+
+
+def test_error_ledger():
+    """test_core.cpp:258-265."""
+    t = T()
+    state = O.random_uniform_mps(6, 2, 6, 55)
+    c1 = t.canonicalize(state.tensors, 0, t.NO_TRUNCATION.with_max_bond(3))
+    c2 = t.canonicalize(c1, 0, t.NO_TRUNCATION.with_max_bond(2))
+    assert c2.error() >= c1.error()
+    assert np.linalg.norm(dense(c2.to_tensors()) - O.mps_to_dense(state)) <= c2.error()
+
+
+def test_norm_and_scprod():
+    t = T()
+    v = O.random_uniform_mps(5, 2, 3, 14)
+    u = O.random_uniform_mps(5, 2, 2, 15)
+    assert abs(t.scprod(v.tensors, v.tensors)[0].real - v.norm_squared()) < 1e-12 * v.norm_squared()
+    assert abs(t.scprod(u.tensors, v.tensors)[0] - np.vdot(O.mps_to_dense(u), O.mps_to_dense(v))) < 1e-12
+    r = I.random_mps(10, 2, 8, 9)
+    assert abs(t.norm(r)[0] - 1.0) < 1e-13
+
+
+# ---------------------------------------------------------------- simplify
+def test_simplify_exact_rank():
+    """test_blas.cpp:41-45."""
+    t = T()
+    v = O.random_uniform_mps(6, 2, 4, 7)
+    s = t.simplify(v.tensors, t.DEFAULT_STRATEGY.with_max_sweeps(6))
+    assert np.linalg.norm(dense(s.to_tensors()) - O.mps_to_dense(v)) < 1e-10 * v.norm()
+
+
+def test_simplify_schmidt_optimum():
+    """test_blas.cpp:46-66 plus oracle parity on the same case."""
+    t = T()
+    v = O.random_uniform_mps(6, 2, 8, 8)
+    d = O.mps_to_dense(v)
+    strat = t.DEFAULT_STRATEGY.with_max_bond(4).with_max_sweeps(12)
+    s = t.simplify(v.tensors, strat)
+    ts = s.to_tensors()
+    assert max(s.bond_dimensions()) <= 4
+    dist = np.linalg.norm(dense(ts) - d)
+    sv = np.linalg.svd(d.reshape(8, 8), compute_uv=False)
+    lower = np.sqrt(np.sum(sv[4:] ** 2))
+    assert dist >= lower - 1e-12
+    assert dist <= 1.10 * max(lower, 1e-14)
+    assert abs(s.error() - dist) < 1e-8 * np.linalg.norm(d)
+    ref = O.simplify(v, O.DEFAULT_STRATEGY.with_max_bond(4).with_max_sweeps(12))
+    assert rel(dense(ts), O.mps_to_dense(ref)) < 1e-10
+    assert abs(s.error() - ref.error) < 1e-10 * np.linalg.norm(d)
+
+
+def test_simplify_guess_accepted():
+    """test_blas.cpp:72-76."""
+    t = T()
+    v = O.random_uniform_mps(5, 2, 3, 10)
+    s = t.simplify(v.tensors, t.DEFAULT_STRATEGY.with_max_sweeps(8), O.basis_state(5, 2, 0).tensors)
+    assert np.linalg.norm(dense(s.to_tensors()) - O.mps_to_dense(v)) < 1e-9 * v.norm()
+
+
+def test_apply_dense_oracle():
+    """test_blas.cpp:109-125."""
+    t = T()
+    from oracle.rng import random_matrix
+    v = O.random_uniform_mps(6, 2, 3, 12)
+    a = O.mpo_sum([1 + 0.5j, -0.3], [O.mpo_from_local_operators([random_matrix(2, 2, s) for s in range(21, 27)]),
+                                     O.mpo_identity(6, 2)])
+    expected = O.mpo_to_dense(a) @ O.mps_to_dense(v)
+    w = t.apply(a.tensors, v.tensors, t.DEFAULT_STRATEGY.with_max_sweeps(8))
+    assert np.linalg.norm(dense(w.to_tensors()) - expected) < 1e-10 * np.linalg.norm(expected)
+    w = t.apply(O.mpo_identity(5, 2).tensors, O.random_uniform_mps(5, 2, 3, 11).tensors)
+    v5 = O.random_uniform_mps(5, 2, 3, 11)
+    assert np.linalg.norm(dense(w.to_tensors()) - O.mps_to_dense(v5)) <= 1e-12 * v5.norm()
+
+
+def _check_config_parity(gpu_out, rep, ref, ref_rep, target_norm, n_dense=True):
+    ts = gpu_out.to_tensors()
+    # 1. bond dims exact
+    assert gpu_out.bond_dimensions() == ref.bond_dimensions()
+    # 3. residual / error vs 1e-10 |T|
+    assert abs(rep["residual"] - ref_rep["residual"]) <= 1e-10 * target_norm
+    # 4. norm
+    nrm = np.linalg.norm(ts[0])
+    assert abs(nrm - ref.norm()) <= 1e-10 * ref.norm()
+    # 6. cancellation-free distance between the two outputs
+    assert distance(ts, ref.tensors) <= 1e-10 * ref.norm()
+    # 7. dense vectors
+    if n_dense:
+        assert rel(dense(ts), O.mps_to_dense(ref)) <= 1e-10
+    # 2. spectra of the final output
+    for s_gpu, s_ref in zip(spectra(ts), spectra(ref.tensors)):
+        assert np.linalg.norm(s_gpu - s_ref) <= 1e-10 * np.linalg.norm(s_ref)
+
+
+def test_config1_simplify_parity():
+    t = T()
+    cfg = I.CONFIGS["C1"]
+    (psi,), _ = I.config_inputs(cfg)
+    strat = t.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
+    rep = []
+    out = t.simplify(psi, strat, report=rep)
+    rrep = {}
+    ref = O.simplify(omps(psi), O.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance,
+                                           max_sweeps=cfg.max_sweeps), report=rrep)
+    assert rep[0]["sweeps"] == rrep["sweeps"]
+    _check_config_parity(out, rep[0], ref, rrep, 1.0)
+
+
+@pytest.mark.slow
+def test_config2_apply_parity():
+    t = T()
+    cfg = I.CONFIGS["C2"]
+    (psi,), W = I.config_inputs(cfg)
+    strat = t.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
+    rep = []
+    out = t.apply(W, psi, strat, report=rep)
+    rrep = {}
+    ref = O.apply(O.MPO(W), omps(psi), O.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance,
+                                                  max_sweeps=cfg.max_sweeps), fast=True, report=rrep)
+    tn = np.sqrt(rrep["target_norm2"])
+    assert abs(rep[0]["target_norm2"] - rrep["target_norm2"]) <= 1e-12 * rrep["target_norm2"]
+    _check_config_parity(out, rep[0], ref, rrep, tn)
+
+
+def test_batched_simplify_matches_single_chains():
+    t = T()
+    chains = [I.random_mps(12, 2, 32, 500 + i) for i in range(6)]
+    strat = t.Strategy(max_bond=12, max_sweeps=4)
+    rep = []
+    out = t.simplify(t.DeviceMPS.from_batch(chains), strat, report=rep)
+    for i, ch in enumerate(chains):
+        rr = {}
+        ref = O.simplify(omps(ch), O.Strategy(max_bond=12, max_sweeps=4), report=rr)
+        ts = out.to_tensors(i)
+        assert out.bond_dimensions(i) == ref.bond_dimensions()
+        assert rel(dense(ts), O.mps_to_dense(ref)) <= 1e-10
+        assert abs(rep[i]["residual"] - rr["residual"]) <= 1e-10
+        assert rep[i]["sweeps"] == rr["sweeps"]
+
+
+def test_complex_hadamard_simplify_small():
+    t = T()
+    a = I.random_mps(10, 2, 6, 303, complex_=True)
+    b = I.random_mps(10, 2, 6, 304, complex_=True)
+    strat = t.Strategy(max_bond=12, tolerance=1e-10)
+    rep = []
+    w = t.hadamard(a, b)
+    out = t.simplify(w, strat, report=rep)
+    rr = {}
+    ref = O.simplify(O.hadamard(omps(a), omps(b)), O.Strategy(max_bond=12, tolerance=1e-10), report=rr)
+    _check_config_parity(out, rep[0], ref, rr, np.sqrt(rr["target_norm2"]))
