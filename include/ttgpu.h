@@ -101,6 +101,14 @@ ttg_status ttg_synchronize(ttg_ctx* ctx);
 int64_t ttg_kernel_launches(const ttg_ctx* ctx);
 const char* ttg_version(void);
 
+/* Per-kernel-class timing: when enabled, every launch is bracketed by CUDA
+ * events on the context stream and GEMM/SVD/QR launches record their executed
+ * flops (read from the device bond table, one host sync per launch: use a
+ * separate pass, not the timed one).  Enabling resets the counters. */
+enum { TTG_PROF_GEMM = 0, TTG_PROF_SVD = 1, TTG_PROF_QR = 2, TTG_PROF_EXPAND = 3, TTG_PROF_CLASSES = 4 };
+ttg_status ttg_profile_enable(ttg_ctx* ctx, int on);
+ttg_status ttg_profile_read(ttg_ctx* ctx, int cls, int64_t* launches, double* ms, double* flops);
+
 /* ---- device MPS / MPO ---------------------------------------------------- */
 /* Upload `count` host MPS of identical length/physical dims/bonds as one batch. */
 ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, ttg_dmps** out);

@@ -46,6 +46,9 @@ SIGNATURES = {
     "ttg_synchronize": (C.c_int, [C.c_void_p]),
     "ttg_kernel_launches": (C.c_int64, [C.c_void_p]),
     "ttg_version": (C.c_char_p, []),
+    "ttg_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "ttg_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double)]),
     "ttg_mps_upload": (C.c_int, [C.c_void_p, C.POINTER(ttg_mps_view), C.c_int, C.POINTER(C.c_void_p)]),
     "ttg_mps_from_device": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_void_p), C.POINTER(C.c_double),

@@ -30,12 +30,60 @@
 
 using namespace ttg;
 
+// Per-kernel-class profile (enabled by ttg_profile_enable): CUDA events around
+// every launch of the engine on the context stream, plus the executed flops of
+// each GEMM / SVD evaluated from the device bond table (which costs a host sync
+// per launch, so profiled runs are separate from timed runs).
+struct ProfileRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double flops;
+};
+
 struct ttg_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
+  int profile = 0;
+  std::vector<ProfileRec> pending;
+  int64_t prof_count[TTG_PROF_CLASSES] = {};
+  double prof_ms[TTG_PROF_CLASSES] = {};
+  double prof_flops[TTG_PROF_CLASSES] = {};
+  void flush_profile() {
+    if (pending.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& r : pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.e0, r.e1);
+      prof_count[r.cls] += 1;
+      prof_ms[r.cls] += ms;
+      prof_flops[r.cls] += r.flops;
+      cudaEventDestroy(r.e0);
+      cudaEventDestroy(r.e1);
+    }
+    pending.clear();
+  }
+};
+
+// RAII: brackets one launch with events when profiling.
+struct ProfScope {
+  ttg_ctx* ctx;
+  ProfileRec rec{};
+  ProfScope(ttg_ctx* c, int cls, double flops = 0.0) : ctx(c) {
+    if (!ctx->profile) return;
+    rec.cls = cls;
+    rec.flops = flops;
+    cudaEventCreate(&rec.e0);
+    cudaEventCreate(&rec.e1);
+    cudaEventRecord(rec.e0, ctx->stream);
+  }
+  ~ProfScope() {
+    if (!ctx->profile) return;
+    cudaEventRecord(rec.e1, ctx->stream);
+    ctx->pending.push_back(rec);
+  }
 };
 
 struct ttg_dmps {
@@ -171,9 +219,30 @@ struct Engine {
 
   int ub(DimExpr e) const { return e.idx < 0 ? e.mult : e.mult * bound[e.idx]; }
 
+  // host copies of the bond table / chain states (profiling only)
+  std::vector<int> hb;
+  std::vector<ChainState> hs;
+  bool live_dims(bool check_active) {
+    if (!ctx->profile) return false;
+    CK(cudaStreamSynchronize(st));
+    hb.resize((size_t)B * ld);
+    CK(cudaMemcpy(hb.data(), d_bonds, hb.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    hs.resize(B);
+    if (check_active && d_state) CK(cudaMemcpy(hs.data(), d_state, B * sizeof(ChainState), cudaMemcpyDeviceToHost));
+    return true;
+  }
+  bool chain_on(int c, bool check_active) const { return !(check_active && d_state) || hs[c].active; }
+
   void G(const void* A, long long sA, const void* Bm, long long sB, void* C, long long sC, DimExpr M, DimExpr N,
          DimExpr K, int opA, int opB, bool check_active, int beta = 0) {
+    double flops = 0.0;
+    if (live_dims(check_active))
+      for (int c = 0; c < B; ++c)
+        if (chain_on(c, check_active))
+          flops += (Scalar<T>::is_complex ? 8.0 : 2.0) * M.eval(hb.data(), c, ld) * (double)N.eval(hb.data(), c, ld) *
+                   K.eval(hb.data(), c, ld);
     GemmParams p{A, Bm, C, sA, sB, sC, M, N, K, d_bonds, ld, check_active ? d_state : nullptr, 1.0, beta};
+    ProfScope ps(ctx, TTG_PROF_GEMM, flops);
     CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st));
     ++ctx->launches;
   }
@@ -200,8 +269,17 @@ struct Engine {
     p.mode = mode;
     p.work = work;
     p.s_work = s_work;
+    double flops = 0.0;  // Golub-Van Loan R-SVD count (U, S, V): 4m^2n + 8mn^2 + 9n^3, m >= n
+    if (live_dims(check_active))
+      for (int c = 0; c < B; ++c)
+        if (chain_on(c, check_active)) {
+          double a = M.eval(hb.data(), c, ld), b = N.eval(hb.data(), c, ld);
+          if (a < b) std::swap(a, b);
+          flops += (Scalar<T>::is_complex ? 4.0 : 1.0) * (4 * a * a * b + 8 * a * b * b + 9 * b * b * b);
+        }
     const int m = ub(M), n = ub(N);
     const int l = mode == 0 ? m : n, k = mode == 0 ? n : m;
+    ProfScope ps(ctx, TTG_PROF_SVD, flops);
     CK(jacobi_svd<T>(p, l, k, B, st));
     ++ctx->launches;
   }
@@ -325,7 +403,11 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     qp.s_work = P.qr_work;
     qp.m = q[k] * d[k];
     qp.n = g[k + 1];
-    CK(householder_qr<T>(qp, B, st));
+    {
+      const double a = std::max(qp.m, qp.n), b = std::min(qp.m, qp.n);
+      ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * B * 4.0 * b * b * (a - b / 3.0));
+      CK(householder_qr<T>(qp, B, st));
+    }
     ++ctx->launches;
     // carried = R * next.right_matrix()  (mps.hpp:202)
     const int nxt = (k == 0 && curp != cbuf[0]) ? 0 : cur ^ 1;
@@ -701,6 +783,27 @@ ttg_status ttg_synchronize(ttg_ctx* ctx) {
 
 int64_t ttg_kernel_launches(const ttg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+ttg_status ttg_profile_enable(ttg_ctx* ctx, int on) {
+  if (!ctx) return TTG_INVALID;
+  ctx->flush_profile();
+  ctx->profile = on ? 1 : 0;
+  for (int c = 0; c < TTG_PROF_CLASSES; ++c) {
+    ctx->prof_count[c] = 0;
+    ctx->prof_ms[c] = 0.0;
+    ctx->prof_flops[c] = 0.0;
+  }
+  return TTG_OK;
+}
+
+ttg_status ttg_profile_read(ttg_ctx* ctx, int cls, int64_t* launches, double* ms, double* flops) {
+  if (!ctx || cls < 0 || cls >= TTG_PROF_CLASSES) return TTG_INVALID;
+  ctx->flush_profile();
+  if (launches) *launches = ctx->prof_count[cls];
+  if (ms) *ms = ctx->prof_ms[cls];
+  if (flops) *flops = ctx->prof_flops[cls];
+  return TTG_OK;
+}
+
 ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, ttg_dmps** out) {
   return guarded(ctx, [&] {
     if (!views || !out || count < 1) throw Error{TTG_INVALID, "null argument"};
@@ -855,6 +958,7 @@ ttg_status ttg_apply_raw(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, tt
     }
     for (int k = 0; k < n; ++k) {
       const size_t welems = (size_t)op->bonds[k] * op->dout[k] * op->din[k] * op->bonds[k + 1];
+      ProfScope ps(ctx, TTG_PROF_EXPAND, 0.0);
       if (dtype == TTG_F64) {
         CK(expand_mpo<double>(static_cast<const double*>(op->site[k]), static_cast<const double*>(V->site[k]),
                               static_cast<double*>(o->site[k]), op->bonds[k], op->dout[k], op->din[k],
@@ -910,6 +1014,7 @@ ttg_status ttg_hadamard(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, ttg_
       o->error[c] = u->error[c] + v->error[c];  // blas.hpp:66
     }
     for (int k = 0; k < n; ++k) {
+      ProfScope ps(ctx, TTG_PROF_EXPAND, 0.0);
       if (dtype == TTG_F64)
         CK(expand_hadamard<double>(static_cast<const double*>(U->site[k]), static_cast<const double*>(V->site[k]),
                                    static_cast<double*>(o->site[k]), U->bond(0, k), u->phys[k], U->bond(0, k + 1),

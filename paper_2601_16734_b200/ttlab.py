@@ -116,6 +116,19 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib.ttg_kernel_launches(self.handle))
 
+    PROFILE_CLASSES = {"gemm": 0, "svd": 1, "qr": 2, "expand": 3}
+
+    def profile_enable(self, on: bool = True):
+        self.check(lib.ttg_profile_enable(self.handle, int(bool(on))))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for name, cls in self.PROFILE_CLASSES.items():
+            n, ms, fl = C.c_int64(), C.c_double(), C.c_double()
+            self.check(lib.ttg_profile_read(self.handle, cls, C.byref(n), C.byref(ms), C.byref(fl)))
+            out[name] = dict(launches=n.value, ms=ms.value, flops=fl.value)
+        return out
+
     def __del__(self):
         try:
             if self.handle:
