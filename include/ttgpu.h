@@ -108,6 +108,8 @@ const char* ttg_version(void);
 enum { TTG_PROF_GEMM = 0, TTG_PROF_SVD = 1, TTG_PROF_QR = 2, TTG_PROF_EXPAND = 3, TTG_PROF_CLASSES = 4 };
 ttg_status ttg_profile_enable(ttg_ctx* ctx, int on);
 ttg_status ttg_profile_read(ttg_ctx* ctx, int cls, int64_t* launches, double* ms, double* flops);
+/* Jacobi sweeps executed by all SVD launches since profiling was enabled. */
+ttg_status ttg_profile_svd_sweeps(ttg_ctx* ctx, int64_t* total);
 
 /* ---- device MPS / MPO ---------------------------------------------------- */
 /* Upload `count` host MPS of identical length/physical dims/bonds as one batch. */
@@ -155,6 +157,10 @@ ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int 
  * mode 1 = RIGHT_TO_LEFT writes V_r^H (r x n); svals[min(m,n)] descending, rank, dropped weight^2. */
 ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
                          void* iso, double* svals, int* rank, double* err2);
+/* As ttg_debug_svd, plus Jacobi sweeps executed, kernel time (ms) and the rotation threshold (0 = default). */
+ttg_status ttg_debug_svd_ex(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
+                            void* iso, double* svals, int* rank, double* err2, int* sweeps, double* ms,
+                            double tol_rot);
 /* Thin Householder QR (mps.hpp:196-199): Q (m x k), R (k x n), k = min(m, n). */
 ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R);
 

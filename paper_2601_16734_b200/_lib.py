@@ -47,6 +47,7 @@ SIGNATURES = {
     "ttg_kernel_launches": (C.c_int64, [C.c_void_p]),
     "ttg_version": (C.c_char_p, []),
     "ttg_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "ttg_profile_svd_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "ttg_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "ttg_mps_upload": (C.c_int, [C.c_void_p, C.POINTER(ttg_mps_view), C.c_int, C.POINTER(C.c_void_p)]),
@@ -74,6 +75,9 @@ SIGNATURES = {
                                  C.c_void_p, C.c_void_p]),
     "ttg_debug_svd": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_int64, C.c_void_p,
                                 C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "ttg_debug_svd_ex": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_int64,
+                                   C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_double]),
     "ttg_debug_qr": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 

@@ -41,7 +41,7 @@ ttg_status do_gemm(int opA, int opB, int M, int N, int K, const void* A, const v
 
 template <typename T>
 ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t max_bond, void* iso, double* svals,
-                  int* rank, double* err2) {
+                  int* rank, double* err2, int* sweeps, double* ms, double tol_rot) {
   const size_t es = sizeof(T);
   const int kmin = m < n ? m : n;
   Buf th((size_t)m * n * es), is((size_t)m * n * es + (size_t)kmin * kmin * es), sv((size_t)kmin * 8),
@@ -68,10 +68,24 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   p.max_bond = max_bond;
   p.mode = mode;
   p.work = work.p;
+  Buf sw(sizeof(int));
+  p.sweeps_out = static_cast<int*>(sw.p);
+  p.tol_rot = tol_rot;
   const int l = mode == 0 ? m : n, k = mode == 0 ? n : m;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, nullptr);
   cudaError_t e = jacobi_svd<T>(p, l, k, 1, nullptr);
+  cudaEventRecord(e1, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return TTG_CUDA;
+  float fms = 0.f;
+  cudaEventElapsedTime(&fms, e0, e1);
+  if (ms) *ms = fms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (sweeps) cudaMemcpy(sweeps, sw.p, sizeof(int), cudaMemcpyDeviceToHost);
   cudaMemcpy(hb, bonds.p, sizeof hb, cudaMemcpyDeviceToHost);
   cudaMemcpy(&z, st.p, sizeof z, cudaMemcpyDeviceToHost);
   const int r = hb[2];
@@ -113,9 +127,16 @@ ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int 
 
 ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
                          void* iso, double* svals, int* rank, double* err2) {
+  return ttg_debug_svd_ex(dtype, m, n, theta, mode, tol, max_bond, iso, svals, rank, err2, nullptr, nullptr, 0.0);
+}
+
+ttg_status ttg_debug_svd_ex(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
+                            void* iso, double* svals, int* rank, double* err2, int* sweeps, double* ms,
+                            double tol_rot) {
   if (m < 1 || n < 1) return TTG_INVALID;
-  return dtype == TTG_F64 ? do_svd<double>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2)
-                          : do_svd<cplx>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2);
+  return dtype == TTG_F64
+             ? do_svd<double>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2, sweeps, ms, tol_rot)
+             : do_svd<cplx>(m, n, theta, mode, tol, max_bond, iso, svals, rank, err2, sweeps, ms, tol_rot);
 }
 
 ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R) {

@@ -51,6 +51,8 @@ struct ttg_ctx {
   int64_t prof_count[TTG_PROF_CLASSES] = {};
   double prof_ms[TTG_PROF_CLASSES] = {};
   double prof_flops[TTG_PROF_CLASSES] = {};
+  int64_t prof_svd_sweeps = 0;
+  int* d_sweeps = nullptr;  // device counter target for the SVD kernel (profiling)
   void flush_profile() {
     if (pending.empty()) return;
     cudaStreamSynchronize(stream);
@@ -247,9 +249,27 @@ struct Engine {
     ++ctx->launches;
   }
 
+  struct Warm {
+    const void* pre = nullptr;
+    long long s_pre = 0;
+    const int* fin = nullptr;
+    int* fout = nullptr;
+    int fld = 0;
+    void* frame = nullptr;
+    long long s_frame = 0;
+  };
+
   void S(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso, long long s_iso,
-         int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work) {
+         int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work,
+         const Warm& w = Warm()) {
     SvdParams p{};
+    p.theta_pre = w.pre;
+    p.s_pre = w.s_pre;
+    p.frame_in = w.fin;
+    p.frame_out = w.fout;
+    p.frame_ld = w.fld;
+    p.frame = w.frame;
+    p.s_frame = w.s_frame;
     p.theta = theta;
     p.s_theta = s_theta;
     p.M = M;
@@ -279,9 +299,22 @@ struct Engine {
         }
     const int m = ub(M), n = ub(N);
     const int l = mode == 0 ? m : n, k = mode == 0 ? n : m;
-    ProfScope ps(ctx, TTG_PROF_SVD, flops);
-    CK(jacobi_svd<T>(p, l, k, B, st));
+    if (ctx->profile) {
+      if (!ctx->d_sweeps) CK(cudaMalloc(&ctx->d_sweeps, 4096 * sizeof(int)));
+      CK(cudaMemsetAsync(ctx->d_sweeps, 0, B * sizeof(int), st));
+      p.sweeps_out = B <= 4096 ? ctx->d_sweeps : nullptr;
+    }
+    {
+      ProfScope ps(ctx, TTG_PROF_SVD, flops);
+      CK(jacobi_svd<T>(p, l, k, B, st));
+    }
     ++ctx->launches;
+    if (ctx->profile && p.sweeps_out) {
+      std::vector<int> hsw(B);
+      CK(cudaMemcpyAsync(hsw.data(), ctx->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int c = 0; c < B; ++c) ctx->prof_svd_sweeps += hsw[c];
+    }
   }
 };
 
@@ -341,7 +374,10 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     P.bcap = std::max(P.bcap, (long long)bound[k + 1] * bound[k + 1]);
     // R->L pass panels: theta = q_k x d p_{k+1}
     const long long l1 = (long long)d[k] * bound[k + 1], k1 = q[k];
-    if ((l1 * k1) * (long long)sizeof(T) + k1 * 12 + 16 > 220 * 1024) P.svd_work = std::max(P.svd_work, l1 * k1);
+    if (!jacobi_svd_panel_in_smem(l1, k1, sizeof(T))) P.svd_work = std::max(P.svd_work, l1 * k1);
+    // pass 3 (centre > 0): left unfolding (bound_k d) x bound_{k+1}
+    const long long l3 = (long long)bound[k] * d[k], k3 = bound[k + 1];
+    if (!jacobi_svd_panel_in_smem(l3, k3, sizeof(T))) P.svd_work = std::max(P.svd_work, l3 * k3);
   }
   for (int n = 0; n + 1 < L; ++n) {
     const long long dn = d[n], dn1 = d[n + 1];
@@ -350,7 +386,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     P.yw = std::max({P.yw, (long long)pb[n] * dn * dn1 * t[n + 2], (long long)t[n] * dn * dn1 * pb[n + 2]});
     P.th = std::max(P.th, (long long)pb[n] * dn * dn1 * pb[n + 2]);
     const long long l = (long long)bound[n] * dn, kk = (long long)dn1 * bound[n + 2];
-    if (l * kk * (long long)sizeof(T) + std::max(l, kk) * 12 + 16 > 220 * 1024)
+    if (!jacobi_svd_panel_in_smem(l, kk, sizeof(T)) || !jacobi_svd_panel_in_smem(kk, l, sizeof(T)))
       P.svd_work = std::max(P.svd_work, l * kk);
   }
   if (L >= 1) P.xz = std::max(P.xz, (long long)t[L - 1] * d[L - 1] * pb[L]);
@@ -498,6 +534,22 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     }
     DevBuf XZ((size_t)B * P.xz * es, st), YW((size_t)B * P.yw * es, st), TH((size_t)B * P.th * es, st);
     const long long sxz = P.xz, syw = P.yw, sth = P.th;
+    // warm-start frames per two-site block n: U (after L->R) and V (after R->L)
+    DevBuf TH2((size_t)B * P.th * es, st);
+    std::vector<long long> fcap(L, 1);
+    std::vector<DevBuf> frameU, frameV;
+    frameU.reserve(L);
+    frameV.reserve(L);
+    for (int n = 0; n + 1 < L; ++n) {
+      const long long side = std::max((long long)bound[n] * d[n], (long long)d[n + 1] * bound[n + 2]);
+      fcap[n] = side * side;
+      frameU.emplace_back((size_t)B * fcap[n] * es, st);
+      frameV.emplace_back((size_t)B * fcap[n] * es, st);
+    }
+    DevBuf fmeta((size_t)2 * B * L * sizeof(int), st);
+    CK(cudaMemsetAsync(fmeta.p, 0, (size_t)2 * B * L * sizeof(int), st));
+    int* fU = fmeta.as<int>();
+    int* fV = fU + (size_t)B * L;
     CK(fill_one<T>(lenv[0].as<T>(), P.env_cap[0], B, st));
     CK(fill_one<T>(renv[L].as<T>(), P.env_cap[L], B, st));
     ctx->launches += 2;
@@ -525,8 +577,19 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
             OP_N, OP_N, true);
         E.G(YW.p, syw, renv[n + 2].p, P.env_cap[n + 2], TH.p, sth, dbond(n, dn * dn1), dbond(n + 2),
             dconst(t[n + 2]), OP_N, OP_T, true);
+        // warm start: theta V_prev (same singular values, same U)
+        E.G(TH.p, sth, frameV[n].p, fcap[n], TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n + 2, dn1), OP_N,
+            OP_N, true);
+        typename Engine<T>::Warm wl;
+        wl.pre = TH2.p;
+        wl.s_pre = sth;
+        wl.fin = fV + n;
+        wl.fout = fU + n;
+        wl.fld = L;
+        wl.frame = frameU[n].p;
+        wl.s_frame = fcap[n];
         E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n], P.psi_cap[n], 0, tol, mb, true, false,
-            svdw.p, P.svd_work);
+            svdw.p, P.svd_work, wl);
         E.G(psi->site[n], P.psi_cap[n], TH.p, sth, psi->site[n + 1], P.psi_cap[n + 1], dbond(n + 1),
             dbond(n + 2, dn1), dbond(n, dn), OP_C, OP_N, true);
         E.G(psi->site[n], P.psi_cap[n], XZ.p, sxz, lenv[n + 1].p, P.env_cap[n + 1], dbond(n + 1),
@@ -540,8 +603,19 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
             true);
         E.G(lenv[n].p, P.env_cap[n], YW.p, syw, TH.p, sth, dbond(n), dbond(n + 2, dn * dn1), dconst(t[n]), OP_N,
             OP_N, true);
+        // warm start: U_prev^H theta (same singular values, same V)
+        E.G(frameU[n].p, fcap[n], TH.p, sth, TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n, dn), OP_C, OP_N,
+            true);
+        typename Engine<T>::Warm wr;
+        wr.pre = TH2.p;
+        wr.s_pre = sth;
+        wr.fin = fU + n;
+        wr.fout = fV + n;
+        wr.fld = L;
+        wr.frame = frameV[n].p;
+        wr.s_frame = fcap[n];
         E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n + 1], P.psi_cap[n + 1], 1, tol, mb, true,
-            false, svdw.p, P.svd_work);
+            false, svdw.p, P.svd_work, wr);
         E.G(TH.p, sth, psi->site[n + 1], P.psi_cap[n + 1], psi->site[n], P.psi_cap[n], dbond(n, dn), dbond(n + 1),
             dbond(n + 2, dn1), OP_N, OP_C, true);
         E.G(psi->site[n + 1], P.psi_cap[n + 1], XZ.p, sxz, renv[n + 1].p, P.env_cap[n + 1], dbond(n + 1),
@@ -765,6 +839,8 @@ ttg_status ttg_create(int device, ttg_ctx** out) {
 void ttg_destroy(ttg_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
+  ctx->flush_profile();
+  if (ctx->d_sweeps) cudaFree(ctx->d_sweeps);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -787,11 +863,18 @@ ttg_status ttg_profile_enable(ttg_ctx* ctx, int on) {
   if (!ctx) return TTG_INVALID;
   ctx->flush_profile();
   ctx->profile = on ? 1 : 0;
+  ctx->prof_svd_sweeps = 0;
   for (int c = 0; c < TTG_PROF_CLASSES; ++c) {
     ctx->prof_count[c] = 0;
     ctx->prof_ms[c] = 0.0;
     ctx->prof_flops[c] = 0.0;
   }
+  return TTG_OK;
+}
+
+ttg_status ttg_profile_svd_sweeps(ttg_ctx* ctx, int64_t* total) {
+  if (!ctx || !total) return TTG_INVALID;
+  *total = ctx->prof_svd_sweeps;
   return TTG_OK;
 }
 

@@ -29,7 +29,28 @@ struct SvdParams {
   int mode;           // 0 = LEFT_TO_RIGHT, 1 = RIGHT_TO_LEFT (schmidt.hpp:81-87)
   void* work;         // global scratch (l*k elements per chain) when the panel exceeds shared memory
   long long s_work;
+  int* sweeps_out;    // nullable: Jacobi sweeps executed per chain (diagnostics)
+  double tol_rot;     // rotation threshold |a^H b| > tol_rot |a||b|; 0 = default l*eps
+  // Warm start.  theta_pre = theta F for mode 0 (F = V frame of the previous
+  // split at this bond) or F^H theta for mode 1 (F = U frame); it has the same
+  // singular values and the same isometry as theta.  It is used only when
+  // frame_in[c*frame_ld] == m == n, i.e. the frame was square and complete.
+  const void* theta_pre;
+  long long s_pre;
+  const int* frame_in;
+  int* frame_out;     // written: m if the full orthonormal frame was stored, else 0
+  int frame_ld;
+  void* frame;        // full normalised frame (l x k row-major, columns sorted by singular value)
+  long long s_frame;
 };
+
+// Shared-memory plan of the SVD kernel: per-column metadata plus, when it fits,
+// the whole l x k working panel.  Otherwise the panel lives in `work`.
+constexpr size_t SVD_SMEM_LIMIT = 220 * 1024;
+inline size_t jacobi_svd_meta_bytes(long long kmax) { return (size_t)kmax * (2 * sizeof(double) + sizeof(int)) + 16; }
+inline bool jacobi_svd_panel_in_smem(long long lmax, long long kmax, size_t es) {
+  return jacobi_svd_meta_bytes(kmax) + (size_t)lmax * kmax * es <= SVD_SMEM_LIMIT;
+}
 
 template <typename T>
 cudaError_t jacobi_svd(const SvdParams& p, int lmax, int kmax, int chains, cudaStream_t s);

@@ -127,6 +127,9 @@ class Context:
             n, ms, fl = C.c_int64(), C.c_double(), C.c_double()
             self.check(lib.ttg_profile_read(self.handle, cls, C.byref(n), C.byref(ms), C.byref(fl)))
             out[name] = dict(launches=n.value, ms=ms.value, flops=fl.value)
+        sw = C.c_int64()
+        self.check(lib.ttg_profile_svd_sweeps(self.handle, C.byref(sw)))
+        out["svd"]["jacobi_sweeps"] = sw.value
         return out
 
     def __del__(self):
