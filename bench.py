@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--chains", type=int, default=None, help="batch configs: total chains (default: config)")
     return ap.parse_args()
 
 
@@ -104,11 +105,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def workload(cfg_name, rank):
+def workload(cfg_name, rank, world=1, chains=None):
     from paper_2601_16734_b200 import inputs as I
+    from paper_2601_16734_b200.batch import shard_range
     cfg = I.CONFIGS[cfg_name]
+    if cfg.kind == "batch":
+        total = chains or cfg.batch
+        lo, hi = shard_range(total, world, rank)
+        return cfg, [I.config_inputs(cfg, chain=c)[0][0] for c in range(lo, hi)], None
     if cfg.kind != "apply":
-        raise SystemExit(f"bench workload must be an apply config, got {cfg_name}")
+        raise SystemExit(f"bench workload must be an apply or batch config, got {cfg_name}")
     import dataclasses
     cfg_r = dataclasses.replace(cfg, seed=cfg.seed + 1000 * rank)
     (psi,), W = I.config_inputs(cfg_r)
@@ -137,8 +143,27 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    cfg, psi, W = workload(args.config, 0)
     threads = os.cpu_count() or 1
+    from paper_2601_16734_b200 import inputs as I
+    cfg = I.CONFIGS[args.config]
+    if cfg.kind == "batch":  # each step: `threads` chains on a pool of single-threaded workers
+        t_all, sw_all = 0.0, 0.0
+        for _ in range(args.steps):
+            v, cps, dt = cpu_reference_batch(cfg, threads, threads)
+            t_all += dt
+            sw_all += v * dt
+        val, dt = sw_all / t_all, t_all
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "sweeps/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+                "config": {"workload": f"{cfg.name} batched simplify (sample of {threads} chains per step)",
+                           "parallelism": f"{threads} single-threaded host workers"},
+                "cpu_baseline": {"value": val, "unit": "sweeps/s", "cores": threads, "kind": "port",
+                                 "sample": f"{args.steps} x {threads} chains, oracle/ in reference arithmetic"},
+                "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    cfg, psi, W = workload(args.config, 0)
     val, dt, sweeps = cpu_reference(cfg, psi, W, args.steps, min(args.warmup, 1), threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "sweeps/s", "n_gpus": args.gpus,
@@ -312,10 +337,158 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _cpu_chain(args_):
+    """One chain of the batched config through the oracle (single-threaded worker)."""
+    chain, cfgname = args_
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import ttlab_oracle as O
+    from paper_2601_16734_b200 import inputs as I
+    cfg = I.CONFIGS[cfgname]
+    (psi,), _ = I.config_inputs(cfg, chain=chain)
+    rep = {}
+    t0 = time.perf_counter()
+    O.simplify(O.MPS(psi), O.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps),
+               promote=True, report=rep)
+    return rep["sweeps"], time.perf_counter() - t0
+
+
+def cpu_reference_batch(cfg, nchains, threads):
+    """A pool of `threads` single-threaded oracle workers over `nchains` chains
+    (BASELINE.md CPU plan for config 5); returns (sweeps/s, chains/s, seconds)."""
+    import multiprocessing as mpr
+    t0 = time.perf_counter()
+    with mpr.get_context("spawn").Pool(threads, initializer=_pin_blas) as pool:
+        res = pool.map(_cpu_chain, [(c, cfg.name) for c in range(nchains)])
+    dt = time.perf_counter() - t0
+    return sum(r[0] for r in res) / dt, nchains / dt, dt
+
+
+def _pin_blas():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+
+
+def run_ours_batch(args):
+    """Config 5: independent chains sharded over ranks, one batched simplify per
+    step on each GPU, per-chain (norm, error, sweeps) all-gathered over NCCL."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_16734_b200 import ttlab
+    from paper_2601_16734_b200.batch import gather_chain_stats
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    total = args.chains or None
+    cfg, chains, _ = workload(args.config, rank, world, total)
+    total = args.chains or cfg.batch
+    strat = ttlab.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
+    ctx = ttlab.context(local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    batch = ttlab.DeviceMPS.from_batch(chains, ctx=ctx)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(target):
+        reps = []
+        out = ttlab.simplify(target, strat, report=reps)
+        st = torch.tensor([[r["norm"], r["error"], float(r["sweeps"])] for r in reps], dtype=torch.float64,
+                          device=dev)
+        allst = gather_chain_stats(st, total, world)
+        return out, reps, allst
+
+    for _ in range(args.warmup):
+        step(batch)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.kernel_launches
+    sweeps = 0
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        out, reps, allst = step(batch)
+        ev[i][1].record(stream)
+        sweeps += int(allst[:, 2].sum().item())
+    torch.cuda.synchronize()
+    barrier()
+    launches = ctx.kernel_launches - launches0
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+
+    # e2e: host chains in, host chains out
+    h2d = sum(a.nbytes for ch in chains for a in ch)
+    barrier()
+    t_e2e, e2e_sweeps, d2h = 0.0, 0, 0
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out, reps, allst = step(ttlab.DeviceMPS.from_batch(chains, ctx=ctx))
+        res = [out.to_tensors(c) for c in range(len(chains))]
+        t_e2e += time.perf_counter() - t0
+        e2e_sweeps += int(allst[:, 2].sum().item())
+        d2h = sum(a.nbytes for ch in res for a in ch)
+    ms_t = torch.tensor([ms, t_e2e * 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max, e2e_ms_max = float(ms_t[0]), float(ms_t[1])
+    value = sweeps / (ms_max / 1e3)
+    e2e_value = e2e_sweeps / (e2e_ms_max / 1e3)
+    prof = None
+    if not args.no_profile:
+        ctx.profile_enable(True)
+        step(batch)
+        prof = ctx.profile_read()
+        ctx.profile_enable(False)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, cps, dt = cpu_reference_batch(cfg, threads, threads)
+        cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port", "chains_per_s": cps,
+               "sample": f"{threads} chains of {cfg.name} on a pool of {threads} single-threaded workers "
+                         f"({dt:.1f} s), oracle/ in reference arithmetic (complex128)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.chains is None and world == 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {total} independent n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS "
+                                   f"(seeds {cfg.seed}+i), simplify to chi={cfg.out_chi}, tol {cfg.tolerance:g}, "
+                                   f"max {cfg.max_sweeps} sweeps", "global_batch": total,
+                       "chains_per_gpu": len(chains), "parallelism": f"dp{world} (chain shards, NCCL all-gather "
+                                                                      "of per-chain norm/error/sweeps)",
+                       "l2": "flushed between steps (512 MiB write)"},
+            "chains_per_s": total * args.steps / (ms_max / 1e3),
+            "e2e": {"value": e2e_value, "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches), "profile": prof, "cpu_baseline": cpu, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    from paper_2601_16734_b200 import inputs as I
+    batch = I.CONFIGS[args.config].kind == "batch"
     if args.impl == "reference":
         run_reference(args)
+    elif batch:
+        run_ours_batch(args)
     else:
         run_ours(args)
 

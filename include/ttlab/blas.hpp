@@ -1,0 +1,33 @@
+// Drop-in ttlab/blas.hpp hot-path entries on the B200:
+// apply(MPO, MPS, Strategy) (/root/reference/proj/include/ttlab/blas.hpp:8-11) and
+// hadamard(MPS, MPS) (:45-67).
+#pragma once
+
+#include "ttlab/simplify.hpp"
+
+namespace ttlab {
+
+inline CanonicalMPS apply(const MPO& op, const MPS& v, const Strategy& strategy = DEFAULT_STRATEGY) {
+  if (op.size() != v.size()) throw shape_error("apply: operator and state sizes differ");
+  auto w = gpu::upload(op);
+  auto d = gpu::upload(v);
+  const ttg_strategy s = gpu::to_c(strategy);
+  ttg_dmps* out = nullptr;
+  gpu::check(gpu::ctx(), ttg_apply(gpu::ctx(), w.h, d.h, &s, &out, nullptr));
+  gpu::DMps o(out);
+  return gpu::canonical_from(o.h, 0);
+}
+
+inline MPS hadamard(const MPS& u, const MPS& v) {
+  if (u.size() != v.size()) throw shape_error("hadamard: states of different length");
+  auto du = gpu::upload(u);
+  auto dv = gpu::upload(v);
+  ttg_dmps* out = nullptr;
+  gpu::check(gpu::ctx(), ttg_hadamard(gpu::ctx(), du.h, dv.h, &out));
+  gpu::DMps o(out);
+  double err = 0.0;
+  auto ts = gpu::download(o.h, 0, &err, nullptr);
+  return MPS(std::move(ts), err);
+}
+
+}  // namespace ttlab

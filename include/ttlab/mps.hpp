@@ -1,0 +1,163 @@
+// Drop-in restatement of the MPS containers of ttlab/mps.hpp
+// (/root/reference/proj/include/ttlab/mps.hpp:21-143, 180-323, 416-449, 493-544).
+// Containers keep the reference's value semantics and host storage; every
+// numerical operation on the hot path (canonical form, norms, overlaps)
+// executes on the B200 through the C ABI (include/ttgpu.h, see gpu.hpp).
+#pragma once
+
+#include <algorithm>
+#include <random>
+#include <vector>
+
+#include "ttlab/tensor.hpp"
+#include "ttlab/types.hpp"
+
+namespace ttlab {
+
+inline constexpr index_t DENSE_VECTOR_GUARD = index_t(1) << 26;
+
+class MPS {
+public:
+  MPS() = default;
+  explicit MPS(std::vector<Tensor3> tensors, double error = 0.0) : tensors_(std::move(tensors)), error_(error) {
+    check_shape();
+  }
+  index_t size() const { return static_cast<index_t>(tensors_.size()); }
+  const Tensor3& operator[](index_t n) const { return tensors_[static_cast<size_t>(n)]; }
+  Tensor3& operator[](index_t n) { return tensors_[static_cast<size_t>(n)]; }
+  const std::vector<Tensor3>& tensors() const { return tensors_; }
+  std::vector<index_t> physical_dimensions() const {
+    std::vector<index_t> d;
+    for (const auto& t : tensors_) d.push_back(t.phys_dim());
+    return d;
+  }
+  std::vector<index_t> bond_dimensions() const {
+    std::vector<index_t> d{tensors_.empty() ? 1 : tensors_.front().left_dim()};
+    for (const auto& t : tensors_) d.push_back(t.right_dim());
+    return d;
+  }
+  index_t max_bond_dimension() const {
+    index_t chi = 1;
+    for (const auto& t : tensors_) chi = std::max({chi, t.left_dim(), t.right_dim()});
+    return chi;
+  }
+  index_t dimension(index_t guard = DENSE_VECTOR_GUARD) const {
+    index_t dim = 1;
+    for (const auto& t : tensors_) {
+      dim *= t.phys_dim();
+      if (dim > guard) throw capacity_error("MPS dimension exceeds guard");
+    }
+    return dim;
+  }
+  double error() const { return error_; }
+  void set_error(double e) { error_ = e; }
+  double update_error(double delta) { return error_ += delta; }
+  double norm_squared() const;  // <v,v> on the device (gpu.hpp)
+  double norm() const { return std::sqrt(std::max(0.0, norm_squared())); }
+
+protected:
+  void check_shape() const {
+    if (tensors_.empty()) return;
+    if (tensors_.front().left_dim() != 1 || tensors_.back().right_dim() != 1)
+      throw shape_error("MPS boundary bonds must have size one");
+    for (size_t n = 0; n + 1 < tensors_.size(); ++n)
+      if (tensors_[n].right_dim() != tensors_[n + 1].left_dim())
+        throw shape_error("MPS bond mismatch between neighboring tensors");
+    if (error_ < 0) throw shape_error("MPS error bound must be non-negative");
+  }
+  std::vector<Tensor3> tensors_;
+  double error_ = 0.0;
+};
+
+/// MPS in canonical form around `center` (off-centre tensors are isometries).
+class CanonicalMPS : public MPS {
+public:
+  CanonicalMPS() = default;
+  CanonicalMPS(std::vector<Tensor3> tensors, index_t center, double error)
+      : MPS(std::move(tensors), error), center_(center) {}
+  /// mps.hpp:188-218 on the device (QR pass + truncating right-to-left pass).
+  CanonicalMPS(const MPS& state, index_t center, const Strategy& strategy);
+  index_t center() const { return center_; }
+  double norm_squared() const {
+    const double n = tensors_[static_cast<size_t>(center_)].frobenius_norm();
+    return n * n;
+  }
+  double norm() const { return tensors_[static_cast<size_t>(center_)].frobenius_norm(); }
+
+private:
+  index_t center_ = 0;
+};
+
+inline CanonicalMPS canonicalize(const MPS& state, index_t center = 0, const Strategy& strategy = DEFAULT_STRATEGY) {
+  return CanonicalMPS(state, center, strategy);
+}
+
+cplx scprod(const MPS& u, const MPS& v);  // mps.hpp:416-423 (device)
+inline double norm(const MPS& s) { return s.norm(); }
+inline double norm(const CanonicalMPS& s) { return s.norm(); }
+
+/// Dense vector (mps.hpp:438-449), most significant site first.
+inline std::vector<cplx> mps_to_dense(const MPS& state, index_t guard = DENSE_VECTOR_GUARD) {
+  const index_t dim = state.dimension(guard);
+  std::vector<cplx> acc{cplx(1)};
+  index_t rows = 1;
+  for (index_t n = 0; n < state.size(); ++n) {
+    const Tensor3& t = state[n];
+    const index_t a = t.left_dim(), w = t.phys_dim() * t.right_dim();
+    std::vector<cplx> next(static_cast<size_t>(rows * w), cplx(0));
+    for (index_t r = 0; r < rows; ++r)
+      for (index_t k = 0; k < a; ++k) {
+        const cplx x = acc[static_cast<size_t>(r * a + k)];
+        if (x == cplx(0)) continue;
+        for (index_t j = 0; j < w; ++j) next[static_cast<size_t>(r * w + j)] += x * t.data()[k * w + j];
+      }
+    rows *= t.phys_dim();
+    acc = std::move(next);
+  }
+  if (rows != dim) throw shape_error("mps_to_dense: inconsistent contraction");
+  return acc;
+}
+
+/// random_uniform_mps (mps.hpp:493-514): entries cplx(U(-1,1), U(-1,1)) from
+/// std::mt19937_64(seed), interior bonds min(bond, d^k, d^(L-k)).
+inline MPS random_uniform_mps(index_t L, index_t d, index_t bond, uint64_t seed) {
+  if (L < 1 || d < 1 || bond < 1) throw shape_error("random_uniform_mps: L, d, bond must be >= 1");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  auto cap = [&](index_t cut) {
+    const double c = std::min({static_cast<double>(bond), std::pow(static_cast<double>(d), static_cast<double>(cut)),
+                               std::pow(static_cast<double>(d), static_cast<double>(L - cut))});
+    return static_cast<index_t>(std::max(1.0, c));
+  };
+  std::vector<Tensor3> ts;
+  for (index_t n = 0; n < L; ++n) {
+    Tensor3 t(cap(n), d, cap(n + 1));
+    for (index_t i = 0; i < t.size(); ++i) t.data()[i] = cplx(dist(rng), dist(rng));
+    ts.push_back(std::move(t));
+  }
+  return MPS(std::move(ts), 0.0);
+}
+
+inline MPS basis_state(index_t L, index_t d, index_t idx) {
+  std::vector<Tensor3> ts(static_cast<size_t>(L));
+  index_t rem = idx;
+  for (index_t n = L - 1; n >= 0; --n) {
+    Tensor3 t(1, d, 1);
+    t(0, rem % d, 0) = 1.0;
+    ts[static_cast<size_t>(n)] = std::move(t);
+    rem /= d;
+  }
+  return MPS(std::move(ts), 0.0);
+}
+
+inline MPS product_state(index_t L, const std::vector<cplx>& site) {
+  std::vector<Tensor3> ts;
+  for (index_t n = 0; n < L; ++n) {
+    Tensor3 t(1, static_cast<index_t>(site.size()), 1);
+    for (size_t s = 0; s < site.size(); ++s) t(0, static_cast<index_t>(s), 0) = site[s];
+    ts.push_back(std::move(t));
+  }
+  return MPS(std::move(ts), 0.0);
+}
+
+}  // namespace ttlab
