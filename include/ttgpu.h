@@ -153,6 +153,9 @@ ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double
 /* C[b] = op(A[b]) op(B[b]) for b < batch; op: 0 = N, 1 = T, 2 = C (conj-transpose), 3 = conj. */
 ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A, const void* B,
                           void* C);
+/* Same GEMM on device buffers, `reps` back-to-back launches; average kernel time in ms. */
+ttg_status ttg_debug_gemm_dev(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A,
+                              const void* B, void* C, int reps, double* ms);
 /* schmidt_split (schmidt.hpp:72-89) of one m x n theta: mode 0 = LEFT_TO_RIGHT writes U_r (m x r),
  * mode 1 = RIGHT_TO_LEFT writes V_r^H (r x n); svals[min(m,n)] descending, rank, dropped weight^2. */
 ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,
@@ -163,6 +166,8 @@ ttg_status ttg_debug_svd_ex(int dtype, int m, int n, const void* theta, int mode
                             double tol_rot);
 /* Thin Householder QR (mps.hpp:196-199): Q (m x k), R (k x n), k = min(m, n). */
 ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R);
+/* Same factorisation through the blocked path (panel kernel + DMMA WY updates). */
+ttg_status ttg_debug_qr_blocked(int dtype, int m, int n, const void* A, void* Q, void* R);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -114,15 +114,62 @@ ttg_status do_qr(int m, int n, const void* A, void* Q, void* R) {
   return TTG_OK;
 }
 
+template <typename T>
+ttg_status do_qr_blocked(int m, int n, const void* A, void* Q, void* R) {
+  const size_t es = sizeof(T);
+  const int k = m < n ? m : n;
+  size_t sA, sV, sT, sW, sP;
+  qr_blocked_elems<T>(m, n, &sA, &sV, &sT, &sW, &sP);
+  Buf a((size_t)m * n * es), q((size_t)m * k * es), r((size_t)k * n * es), wa(sA * es), wv(sV * es), wt(sT * es),
+      w1(sW * es), w2(sW * es), wp(sP * es);
+  cudaMemcpy(a.p, A, (size_t)m * n * es, cudaMemcpyHostToDevice);
+  QrParams p{a.p, 0, q.p, 0, r.p, 0, nullptr, 0, m, n};
+  QrBlockedWork w{wa.p, wv.p, wt.p, w1.p, w2.p, wp.p, 0, 0, 0, 0, 0};
+  cudaError_t e = householder_qr_blocked<T>(p, w, 1, nullptr, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return TTG_CUDA;
+  cudaMemcpy(Q, q.p, (size_t)m * k * es, cudaMemcpyDeviceToHost);
+  cudaMemcpy(R, r.p, (size_t)k * n * es, cudaMemcpyDeviceToHost);
+  return TTG_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+ttg_status ttg_debug_qr_blocked(int dtype, int m, int n, const void* A, void* Q, void* R) {
+  if (m < 1 || n < 1) return TTG_INVALID;
+  return dtype == TTG_F64 ? do_qr_blocked<double>(m, n, A, Q, R) : do_qr_blocked<cplx>(m, n, A, Q, R);
+}
+
 
 ttg_status ttg_debug_gemm(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A, const void* B,
                           void* C) {
   if (M < 1 || N < 1 || K < 0 || batch < 1) return TTG_INVALID;
   return dtype == TTG_F64 ? do_gemm<double>(opA, opB, M, N, K, A, B, C, batch)
                           : do_gemm<cplx>(opA, opB, M, N, K, A, B, C, batch);
+}
+
+ttg_status ttg_debug_gemm_dev(int dtype, int opA, int opB, int M, int N, int K, int batch, const void* A,
+                              const void* B, void* C, int reps, double* ms) {
+  if (M < 1 || N < 1 || K < 0 || batch < 1 || reps < 1) return TTG_INVALID;
+  const long long na = (long long)M * K, nb = (long long)K * N, nc = (long long)M * N;
+  GemmParams p{A, B, C, na, nb, nc, dconst(M), dconst(N), dconst(K), nullptr, 0, nullptr, 1.0, 0};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaError_t e = cudaSuccess;
+  cudaEventRecord(e0, nullptr);
+  for (int r = 0; r < reps && e == cudaSuccess; ++r)
+    e = dtype == TTG_F64 ? gemm<double>(p, opA, opB, M, N, batch, nullptr) : gemm<cplx>(p, opA, opB, M, N, batch, nullptr);
+  cudaEventRecord(e1, nullptr);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float f = 0.f;
+  cudaEventElapsedTime(&f, e0, e1);
+  if (ms) *ms = f / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return e == cudaSuccess ? TTG_OK : TTG_CUDA;
 }
 
 ttg_status ttg_debug_svd(int dtype, int m, int n, const void* theta, int mode, double tol, int64_t max_bond,

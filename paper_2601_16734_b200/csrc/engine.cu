@@ -322,6 +322,7 @@ struct Engine {
 struct Plan {
   std::vector<long long> psi_cap;
   long long ccap = 1, rcap = 1, bcap = 1, svd_work = 0, qr_work = 0;
+  long long qb_A = 0, qb_V = 0, qb_T = 0, qb_W = 0, qb_P = 0;  // blocked-QR workspaces
   long long xz = 1, yw = 1, th = 1;
   std::vector<long long> env_cap;
 };
@@ -368,7 +369,15 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     if (k + 1 < L) {
       P.rcap = std::max(P.rcap, (long long)q[k + 1] * gk1);
       const long long qw = (long long)qr_workspace_elems<T>(q[k] * d[k], (int)gk1);
-      if (qw * (long long)sizeof(T) > 200 * 1024) P.qr_work = std::max(P.qr_work, qw);
+      if (qw * (long long)sizeof(T) > 200 * 1024) {  // blocked path (panel kernel + DMMA WY updates)
+        size_t a, v, t2, w, pp;
+        qr_blocked_elems<T>(q[k] * d[k], (int)gk1, &a, &v, &t2, &w, &pp);
+        P.qb_A = std::max(P.qb_A, (long long)a);
+        P.qb_V = std::max(P.qb_V, (long long)v);
+        P.qb_T = std::max(P.qb_T, (long long)t2);
+        P.qb_W = std::max(P.qb_W, (long long)w);
+        P.qb_P = std::max(P.qb_P, (long long)pp);
+      }
     }
     P.bcap = std::max(P.bcap, (long long)q[k] * std::min<long long>(q[k], (long long)d[k] * bound[k + 1]));
     P.bcap = std::max(P.bcap, (long long)bound[k + 1] * bound[k + 1]);
@@ -413,6 +422,11 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   DevBuf C0((size_t)B * P.ccap * es, st), C1((size_t)B * P.ccap * es, st);
   DevBuf Rb((size_t)B * P.rcap * es, st), Bb((size_t)B * P.bcap * es, st);
   DevBuf qrw(P.qr_work ? (size_t)B * P.qr_work * es : 0, st);
+  const bool any_blocked = P.qb_A > 0;
+  DevBuf qbA(any_blocked ? (size_t)B * P.qb_A * es : 0, st), qbV(any_blocked ? (size_t)B * P.qb_V * es : 0, st),
+      qbT(any_blocked ? (size_t)B * P.qb_T * es : 0, st), qbW1(any_blocked ? (size_t)B * P.qb_W * es : 0, st),
+      qbW2(any_blocked ? (size_t)B * P.qb_W * es : 0, st), qbP(any_blocked ? (size_t)B * P.qb_P * es : 0, st);
+  const QrBlockedWork qbw{qbA.p, qbV.p, qbT.p, qbW1.p, qbW2.p, qbP.p, P.qb_A, P.qb_V, P.qb_T, P.qb_W, P.qb_P};
   DevBuf svdw(P.svd_work ? (size_t)B * P.svd_work * es : 0, st);
   const long long sC = P.ccap, sR = P.rcap, sBb = P.bcap;
   T* cbuf[2] = {C0.as<T>(), C1.as<T>()};
@@ -442,7 +456,13 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     {
       const double a = std::max(qp.m, qp.n), b = std::min(qp.m, qp.n);
       ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * B * 4.0 * b * b * (a - b / 3.0));
-      CK(householder_qr<T>(qp, B, st));
+      if ((long long)qr_workspace_elems<T>(qp.m, qp.n) * (long long)sizeof(T) > 200 * 1024) {
+        long long nl = 0;
+        CK(householder_qr_blocked<T>(qp, qbw, B, st, &nl));
+        ctx->launches += nl - 1;
+      } else {
+        CK(householder_qr<T>(qp, B, st));
+      }
     }
     ++ctx->launches;
     // carried = R * next.right_matrix()  (mps.hpp:202)

@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
   const int m0 = tm * BM, n0 = tn * BN;
   if (m0 >= M || n0 >= N) return;
 
+  const long long lda = p.lda ? p.lda : ((OPA == OP_N || OPA == OP_R) ? K : M);
+  const long long ldb = p.ldb ? p.ldb : ((OPB == OP_N || OPB == OP_R) ? N : K);
+  const long long ldc = p.ldc ? p.ldc : N;
   const T* A = static_cast<const T*>(p.A) + p.sA * chain;
   const T* B = static_cast<const T*>(p.B) + p.sB * chain;
   T* C = static_cast<T*>(p.C) + p.sC * chain;
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       for (int i = 0; i < BM * BK / NTHREADS; ++i) {
         const int m = mb + (NTHREADS / BK) * i;
         const bool v = (m0 + m < M) && (k0 + kk < K);
-        const T* src = v ? A + (long long)(m0 + m) * K + (k0 + kk) : A;
+        const T* src = v ? A + (m0 + m) * lda + (k0 + kk) : A;
         cp_async(&As[stage][kk][m], src, v, sizeof(T));
       }
     } else {
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       for (int i = 0; i < BK / 2; ++i) {
         const int kk = kb + 2 * i;
         const bool v = (m0 + m < M) && (k0 + kk < K);
-        const T* src = v ? A + (long long)(k0 + kk) * M + (m0 + m) : A;
+        const T* src = v ? A + (k0 + kk) * lda + (m0 + m) : A;
         cp_async(&As[stage][kk][m], src, v, sizeof(T));
       }
     }
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       for (int i = 0; i < BK / 2; ++i) {
         const int kk = kb + 2 * i;
         const bool v = (n0 + n < N) && (k0 + kk < K);
-        const T* src = v ? B + (long long)(k0 + kk) * N + (n0 + n) : B;
+        const T* src = v ? B + (k0 + kk) * ldb + (n0 + n) : B;
         cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
       }
     } else {
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       for (int i = 0; i < BN * BK / NTHREADS; ++i) {
         const int n = nb + (NTHREADS / BK) * i;
         const bool v = (n0 + n < N) && (k0 + kk < K);
-        const T* src = v ? B + (long long)(n0 + n) * K + (k0 + kk) : B;
+        const T* src = v ? B + (n0 + n) * ldb + (k0 + kk) : B;
         cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
       }
     }
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int m = m0 + wm + i * 16 + g + (r >= 2 ? 8 : 0);
         const int n = n0 + wn + j * 8 + 2 * t4 + (r & 1);
         if (m < M && n < N) {
-          T* dst = C + (long long)m * N + n;
+          T* dst = C + m * ldc + n;
           if constexpr (!CPX) {
             const double v = alpha * acc[i][j][r];
             *dst = p.beta ? *dst + v : v;

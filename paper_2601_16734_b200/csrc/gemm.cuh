@@ -24,6 +24,8 @@ struct GemmParams {
   const ChainState* st;  // nullable: chains with st[c].active == 0 are skipped
   double alpha;
   int beta;  // 0: C = alpha*op(A)op(B); 1: C += alpha*op(A)op(B)
+  // leading dimensions (row strides, elements) of the stored A, B, C; 0 = compact
+  long long lda = 0, ldb = 0, ldc = 0;
 };
 
 // Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only).

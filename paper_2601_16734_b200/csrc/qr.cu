@@ -198,3 +198,288 @@ template cudaError_t householder_qr<double>(const QrParams&, int, cudaStream_t);
 template cudaError_t householder_qr<cplx>(const QrParams&, int, cudaStream_t);
 
 }  // namespace ttg
+
+// ---------------------------------------------------------------------------
+// blocked QR
+// ---------------------------------------------------------------------------
+#include "gemm.cuh"
+
+namespace ttg {
+namespace {
+
+constexpr int PANEL_THREADS = 512;
+
+// Factor the mp x jb panel A[j0:, j0:j0+jb] (row stride lda) in place, write the
+// unit lower-trapezoidal V into Vall[j0:, j0:j0+jb] (row stride k) and the
+// jb x jb upper-triangular WY factor into Tp.
+template <typename T>
+__global__ void __launch_bounds__(PANEL_THREADS) qr_panel_kernel(T* A, long long sA, int lda, int mp, int jb, T* Vall,
+                                                                  long long sV, int ldv, T* Tall, long long sT,
+                                                                  T* Pg, long long sP, int in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[33];
+  __shared__ T s_tau;
+  __shared__ T taus[QR_NB];
+  __shared__ T S[QR_NB][QR_NB + 1];
+  const int chain = blockIdx.x;
+  A += sA * chain;
+  Vall += sV * chain;
+  T* Tp = Tall + sT * chain;
+  T* P = in_smem ? reinterpret_cast<T*>(smem_raw) : Pg + sP * chain;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+
+  for (int idx = tid; idx < mp * jb; idx += blockDim.x) {
+    const int r = idx / jb, c = idx % jb;
+    P[(size_t)c * mp + r] = A[(size_t)r * lda + c];
+  }
+  __syncthreads();
+  for (int j = 0; j < jb && j < mp; ++j) {
+    T* v = P + (size_t)j * mp;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < mp; i += blockDim.x) part += abs2(v[i]);
+    const double xn2 = block_sum(part, red);
+    if (tid == 0) {
+      const T alpha = v[j];
+      double ar, ai;
+      if constexpr (Scalar<T>::is_complex) {
+        ar = alpha.x;
+        ai = alpha.y;
+      } else {
+        ar = alpha;
+        ai = 0.0;
+      }
+      T t = Scalar<T>::zero();
+      if (!(xn2 == 0.0 && ai == 0.0)) {
+        const double beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        if constexpr (Scalar<T>::is_complex) {
+          t = cplx{(beta - ar) / beta, -ai / beta};
+          const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+          red[0] = dr / den;
+          red[1] = -di / den;
+          v[j] = cplx{beta, 0.0};
+        } else {
+          t = (beta - ar) / beta;
+          red[0] = 1.0 / (ar - beta);
+          red[1] = 0.0;
+          v[j] = beta;
+        }
+      } else {
+        red[0] = 1.0;
+        red[1] = 0.0;
+      }
+      s_tau = t;
+      taus[j] = t;
+    }
+    __syncthreads();
+    T sc;
+    if constexpr (Scalar<T>::is_complex)
+      sc = cplx{red[0], red[1]};
+    else
+      sc = red[0];
+    for (int i = j + 1 + tid; i < mp; i += blockDim.x) v[i] = mul(v[i], sc);
+    __syncthreads();
+    const T ct = conj_(s_tau);
+    for (int c = j + 1 + warp; c < jb; c += nwarps) {
+      T* a = P + (size_t)c * mp;
+      T w = Scalar<T>::zero();
+      for (int i = j + lane; i < mp; i += 32) w = add(w, cmul(i == j ? Scalar<T>::one() : v[i], a[i]));
+      if constexpr (Scalar<T>::is_complex) {
+        w.x = warp_sum(w.x);
+        w.y = warp_sum(w.y);
+      } else {
+        w = warp_sum(w);
+      }
+      const T f = mul(ct, w);
+      for (int i = j + lane; i < mp; i += 32) a[i] = sub(a[i], mul(i == j ? Scalar<T>::one() : v[i], f));
+    }
+    __syncthreads();
+  }
+  const int jr = jb < mp ? jb : mp;  // reflectors actually formed
+  // write back R (upper part) and V (unit lower trapezoid, zeros above)
+  for (int idx = tid; idx < mp * jb; idx += blockDim.x) {
+    const int r = idx / jb, c = idx % jb;
+    const T x = P[(size_t)c * mp + r];
+    A[(size_t)r * lda + c] = x;
+    Vall[(size_t)r * ldv + c] = (c >= jr) ? Scalar<T>::zero()
+                                          : (r > c ? x : (r == c ? Scalar<T>::one() : Scalar<T>::zero()));
+  }
+  // S = V^H V (upper part), V read from P
+  for (int pr = warp; pr < jr * jr; pr += nwarps) {
+    const int a = pr / jr, b = pr % jr;
+    if (a >= b) continue;
+    T w = Scalar<T>::zero();
+    for (int i = b + lane; i < mp; i += 32) {
+      const T va = (i == a) ? Scalar<T>::one() : (i > a ? P[(size_t)a * mp + i] : Scalar<T>::zero());
+      const T vb = (i == b) ? Scalar<T>::one() : P[(size_t)b * mp + i];
+      w = add(w, cmul(va, vb));
+    }
+    if constexpr (Scalar<T>::is_complex) {
+      w.x = warp_sum(w.x);
+      w.y = warp_sum(w.y);
+    } else {
+      w = warp_sum(w);
+    }
+    if (lane == 0) S[a][b] = w;
+  }
+  __syncthreads();
+  // xLARFT (forward, columnwise): T[i,i] = tau_i, T[0:i,i] = -tau_i T[0:i,0:i] S[0:i,i]
+  if (tid == 0) {
+    for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
+    for (int i = 0; i < jr; ++i) {
+      const T ti = taus[i];
+      Tp[i * QR_NB + i] = ti;
+      for (int r = 0; r < i; ++r) {
+        T acc = Scalar<T>::zero();
+        for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
+        Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void copy_in_kernel(const T* src, long long s_src, T* dst, long long s_dst, long long n) {
+  const int chain = blockIdx.y;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[s_dst * chain + i] = src[s_src * chain + i];
+}
+
+template <typename T>
+__global__ void upper_kernel(const T* A, long long sA, int n, T* R, long long sR, int k) {
+  const int chain = blockIdx.y;
+  const long long tot = (long long)k * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), c = (int)(idx % n);
+    R[sR * chain + idx] = (c >= i) ? A[sA * chain + idx] : Scalar<T>::zero();
+  }
+}
+
+template <typename T>
+__global__ void eye_kernel(T* Q, long long sQ, int m, int k) {
+  const int chain = blockIdx.y;
+  const long long tot = (long long)m * k;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < tot;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / k), c = (int)(idx % k);
+    Q[sQ * chain + idx] = (i == c) ? Scalar<T>::one() : Scalar<T>::zero();
+  }
+}
+
+int blocks_for(long long n) {
+  long long b = (n + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
+}
+
+}  // namespace
+
+template <typename T>
+size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t* sW, size_t* sP) {
+  const int k = m < n ? m : n;
+  const int nblk = (k + QR_NB - 1) / QR_NB;
+  *sA = (size_t)m * n;
+  *sV = (size_t)m * k;
+  *sT = (size_t)nblk * QR_NB * QR_NB;
+  *sW = (size_t)QR_NB * n;
+  *sP = (size_t)m * QR_NB;
+  return *sA + *sV + *sT + 2 * *sW + *sP;
+}
+
+template <typename T>
+cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, int chains, cudaStream_t s,
+                                   long long* launches) {
+  const int m = p.m, n = p.n, k = m < n ? m : n;
+  if (chains <= 0 || m <= 0 || n <= 0) return cudaSuccess;
+  T* A = static_cast<T*>(w.A);
+  T* V = static_cast<T*>(w.V);
+  T* Tt = static_cast<T*>(w.T);
+  cudaError_t e;
+  long long nl = 0;
+  copy_in_kernel<T><<<dim3(blocks_for((long long)m * n), chains), 256, 0, s>>>(static_cast<const T*>(p.A), p.sA, A,
+                                                                             w.sA, (long long)m * n);
+  ++nl;
+  const size_t panel_bytes_max = (size_t)m * QR_NB * sizeof(T);
+  const size_t smem_limit = 200 * 1024;
+  e = cudaFuncSetAttribute(qr_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
+  if (e != cudaSuccess) return e;
+  (void)panel_bytes_max;
+  for (int j0 = 0; j0 < k; j0 += QR_NB) {
+    const int jb = (k - j0) < QR_NB ? (k - j0) : QR_NB;
+    const int mp = m - j0;
+    const size_t pbytes = (size_t)mp * jb * sizeof(T);
+    const int in_smem = pbytes <= smem_limit;
+    qr_panel_kernel<T><<<chains, PANEL_THREADS, in_smem ? pbytes : 0, s>>>(
+        A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k, Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB,
+        w.sT, static_cast<T*>(w.P), w.sP, in_smem);
+    ++nl;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int nt = n - j0 - jb;
+    if (nt > 0) {
+      // W1 = V^H A_trail (jb x nt)
+      GemmParams g1{V + (size_t)j0 * k + j0, A + (size_t)j0 * n + j0 + jb, w.W1, w.sV, w.sA, w.sW, dconst(jb), dconst(nt),
+                    dconst(mp), nullptr, 0, nullptr, 1.0, 0};
+      g1.lda = k;
+      g1.ldb = n;
+      g1.ldc = nt;
+      if ((e = gemm<T>(g1, OP_C, OP_N, jb, nt, chains, s)) != cudaSuccess) return e;
+      // W2 = T^H W1
+      GemmParams g2{Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(nt),
+                    dconst(jb), nullptr, 0, nullptr, 1.0, 0};
+      g2.lda = QR_NB;
+      g2.ldb = nt;
+      g2.ldc = nt;
+      if ((e = gemm<T>(g2, OP_C, OP_N, jb, nt, chains, s)) != cudaSuccess) return e;
+      // A_trail -= V W2
+      GemmParams g3{V + (size_t)j0 * k + j0, w.W2, A + (size_t)j0 * n + j0 + jb, w.sV, w.sW, w.sA, dconst(mp), dconst(nt),
+                    dconst(jb), nullptr, 0, nullptr, -1.0, 1};
+      g3.lda = k;
+      g3.ldb = nt;
+      g3.ldc = n;
+      if ((e = gemm<T>(g3, OP_N, OP_N, mp, nt, chains, s)) != cudaSuccess) return e;
+      nl += 3;
+    }
+  }
+  upper_kernel<T><<<dim3(blocks_for((long long)k * n), chains), 256, 0, s>>>(A, w.sA, n, static_cast<T*>(p.R), p.sR, k);
+  T* Q = static_cast<T*>(p.Q);
+  eye_kernel<T><<<dim3(blocks_for((long long)m * k), chains), 256, 0, s>>>(Q, p.sQ, m, k);
+  nl += 2;
+  const int nblk = (k + QR_NB - 1) / QR_NB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * QR_NB;
+    const int jb = (k - j0) < QR_NB ? (k - j0) : QR_NB;
+    const int mp = m - j0, kq = k - j0;
+    // W1 = V^H Q_sub (jb x kq)
+    GemmParams g1{V + (size_t)j0 * k + j0, Q + (size_t)j0 * k + j0, w.W1, w.sV, p.sQ, w.sW, dconst(jb), dconst(kq),
+                  dconst(mp), nullptr, 0, nullptr, 1.0, 0};
+    g1.lda = k;
+    g1.ldb = k;
+    g1.ldc = kq;
+    if ((e = gemm<T>(g1, OP_C, OP_N, jb, kq, chains, s)) != cudaSuccess) return e;
+    // W2 = T W1
+    GemmParams g2{Tt + (size_t)b * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(kq), dconst(jb),
+                  nullptr, 0, nullptr, 1.0, 0};
+    g2.lda = QR_NB;
+    g2.ldb = kq;
+    g2.ldc = kq;
+    if ((e = gemm<T>(g2, OP_N, OP_N, jb, kq, chains, s)) != cudaSuccess) return e;
+    // Q_sub -= V W2
+    GemmParams g3{V + (size_t)j0 * k + j0, w.W2, Q + (size_t)j0 * k + j0, w.sV, w.sW, p.sQ, dconst(mp), dconst(kq),
+                  dconst(jb), nullptr, 0, nullptr, -1.0, 1};
+    g3.lda = k;
+    g3.ldb = kq;
+    g3.ldc = k;
+    if ((e = gemm<T>(g3, OP_N, OP_N, mp, kq, chains, s)) != cudaSuccess) return e;
+    nl += 3;
+  }
+  if (launches) *launches += nl;
+  return cudaGetLastError();
+}
+
+template size_t qr_blocked_elems<double>(int, int, size_t*, size_t*, size_t*, size_t*, size_t*);
+template size_t qr_blocked_elems<cplx>(int, int, size_t*, size_t*, size_t*, size_t*, size_t*);
+template cudaError_t householder_qr_blocked<double>(const QrParams&, const QrBlockedWork&, int, cudaStream_t,
+                                                    long long*);
+template cudaError_t householder_qr_blocked<cplx>(const QrParams&, const QrBlockedWork&, int, cudaStream_t,
+                                                  long long*);
+
+}  // namespace ttg

@@ -52,9 +52,11 @@ def test_gemm_ops(dtype, opA, opB):
             assert err < 1e-13, (M, N, K, err)
 
 
+@pytest.mark.parametrize("blocked", [False, True])
 @pytest.mark.parametrize("dtype", [np.float64, np.complex128])
-@pytest.mark.parametrize("shape", [(1, 1), (2, 3), (8, 4), (4, 8), (64, 32), (130, 70), (384, 192), (96, 200)])
-def test_householder_qr(dtype, shape):
+@pytest.mark.parametrize("shape", [(1, 1), (2, 3), (8, 4), (4, 8), (64, 32), (130, 70), (384, 192), (96, 200),
+                                   (1000, 300), (257, 65)])
+def test_householder_qr(dtype, shape, blocked):
     lib = _lib()
     m, n = shape
     k = min(m, n)
@@ -65,7 +67,8 @@ def test_householder_qr(dtype, shape):
     A = np.ascontiguousarray(A)
     Q = np.empty((m, k), dtype=dtype)
     R = np.empty((k, n), dtype=dtype)
-    assert lib.ttg_debug_qr(1 if dtype == np.complex128 else 0, m, n, _ptr(A), _ptr(Q), _ptr(R)) == 0
+    fn = lib.ttg_debug_qr_blocked if blocked else lib.ttg_debug_qr
+    assert fn(1 if dtype == np.complex128 else 0, m, n, _ptr(A), _ptr(Q), _ptr(R)) == 0
     assert np.abs(Q.conj().T @ Q - np.eye(k)).max() < 1e-13
     assert np.abs(Q @ R - A).max() < 1e-12 * max(1, np.abs(A).max())
     assert np.abs(np.tril(R, -1)).max() == 0.0
@@ -78,9 +81,10 @@ def test_qr_rank_deficient():
     Q, R = np.empty((20, 20))[:0], None
     Q = np.empty((40, 20))
     R = np.empty((20, 20))
-    assert lib.ttg_debug_qr(0, 40, 20, _ptr(A), _ptr(Q), _ptr(R)) == 0
-    assert np.abs(Q.T @ Q - np.eye(20)).max() < 1e-13
-    assert np.abs(Q @ R - A).max() < 1e-12 * np.abs(A).max()
+    for fn in (lib.ttg_debug_qr, lib.ttg_debug_qr_blocked):
+        assert fn(0, 40, 20, _ptr(A), _ptr(Q), _ptr(R)) == 0
+        assert np.abs(Q.T @ Q - np.eye(20)).max() < 1e-13
+        assert np.abs(Q @ R - A).max() < 1e-12 * np.abs(A).max()
 
 
 def _svd(theta, mode, tol=0.0, max_bond=0):
