@@ -2,6 +2,7 @@
 // They run exactly the kernels the engine uses, one call each, so the parity
 // tests can pin the GEMM fragment layouts, the QR and the truncated SVD in
 // isolation before the sweep engine is involved.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -45,7 +46,7 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   const size_t es = sizeof(T);
   const int kmin = m < n ? m : n;
   Buf th((size_t)m * n * es), is((size_t)m * n * es + (size_t)kmin * kmin * es), sv((size_t)kmin * 8),
-      bonds(4 * sizeof(int)), st(sizeof(ChainState)), work((size_t)m * n * es);
+      bonds(4 * sizeof(int)), st(sizeof(ChainState)), work((size_t)(m + 1) * (n + 1) * es);
   cudaMemcpy(th.p, theta, (size_t)m * n * es, cudaMemcpyHostToDevice);
   ChainState z{};
   z.active = 1;
@@ -76,7 +77,10 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, nullptr);
-  cudaError_t e = jacobi_svd<T>(p, l, k, 1, nullptr);
+  const char* ge = getenv("TTG_DEBUG_SVD_GRID");
+  const bool use_grid = ge && ge[0] == '1' && jacobi_grid_eligible(l, k, 1, sizeof(T));
+  Buf gw(use_grid ? jacobi_grid_work_bytes(l, k, sizeof(T)) : 16);
+  cudaError_t e = use_grid ? jacobi_svd_grid<T>(p, l, k, 1, gw.p, nullptr) : jacobi_svd<T>(p, l, k, 1, nullptr);
   cudaEventRecord(e1, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return TTG_CUDA;

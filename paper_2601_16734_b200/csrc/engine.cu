@@ -16,6 +16,8 @@
 #include <memory>
 #include <type_traits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -214,6 +216,11 @@ struct Engine {
   int L, B;
   std::vector<int> d, t, g, q, pb, bound;
   int* d_bonds = nullptr;  // B x (L+1) psi bonds
+  void* svd_grid_work = nullptr;  // workspace of the grid-cooperative SVD (few large splits)
+  // QR-preconditioned split (Q1, R1^H, L, U_L per chain, `pre_cap` elements each)
+  void* pre_buf = nullptr;
+  long long pre_cap = 0;
+  int pre_slot = 0;
   int ld = 0;
   ChainState* d_state = nullptr;
 
@@ -259,9 +266,13 @@ struct Engine {
     long long s_frame = 0;
   };
 
+  void split_preconditioned(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso,
+                            long long s_iso, int mode, double tol, int max_bond, bool check_active, bool accumulate,
+                            void* work, long long s_work);
+
   void S(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso, long long s_iso,
          int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work,
-         const Warm& w = Warm()) {
+         const Warm& w = Warm(), bool no_pre = false) {
     SvdParams p{};
     p.theta_pre = w.pre;
     p.s_pre = w.s_pre;
@@ -289,6 +300,19 @@ struct Engine {
     p.mode = mode;
     p.work = work;
     p.s_work = s_work;
+    const int mu = ub(M), nu = ub(N);
+    static const bool pre_ok = [] {
+      const char* e = getenv("TTG_SVD_PRECOND");
+      return !(e && e[0] == '0');
+    }();
+    const bool grid_path = svd_grid_work && jacobi_grid_eligible(mode == 0 ? mu : nu, mode == 0 ? nu : mu, B, sizeof(T));
+    if (!no_pre && pre_ok && pre_buf && !grid_path && w.pre == nullptr && (long long)mu * nu >= 24 * 24 &&
+        (size_t)(std::max(mu, nu) | 1) * std::max(mu, nu) * sizeof(T) <= QR_R_SMEM_LIMIT && std::min(mu, nu) <= 1024 &&
+        (long long)std::max(mu, nu) * std::max(mu, nu) <= pre_cap) {
+      split_preconditioned(theta, s_theta, M, N, out_idx, iso, s_iso, mode, tol, max_bond, check_active, accumulate,
+                           work, s_work);
+      return;
+    }
     double flops = 0.0;  // Golub-Van Loan R-SVD count (U, S, V): 4m^2n + 8mn^2 + 9n^3, m >= n
     if (live_dims(check_active))
       for (int c = 0; c < B; ++c)
@@ -306,7 +330,14 @@ struct Engine {
     }
     {
       ProfScope ps(ctx, TTG_PROF_SVD, flops);
-      CK(jacobi_svd<T>(p, l, k, B, st));
+      static const bool grid_ok = [] {
+        const char* e = getenv("TTG_SVD_GRID");
+        return !(e && e[0] == '0');
+      }();
+      if (grid_ok && svd_grid_work && jacobi_grid_eligible(l, k, B, sizeof(T)))
+        CK(jacobi_svd_grid<T>(p, l, k, B, svd_grid_work, st));
+      else
+        CK(jacobi_svd<T>(p, l, k, B, st));
     }
     ++ctx->launches;
     if (ctx->profile && p.sweeps_out) {
@@ -314,9 +345,43 @@ struct Engine {
       CK(cudaMemcpyAsync(hsw.data(), ctx->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       for (int c = 0; c < B; ++c) ctx->prof_svd_sweeps += hsw[c];
+      static const bool print_sweeps = getenv("TTG_PRINT_SWEEPS") != nullptr;
+      if (print_sweeps)
+        fprintf(stderr, "svd mode=%d l<=%d k<=%d warm=%d sweeps=%d\n", mode, l, k, w.pre != nullptr ? 1 : 0, hsw[0]);
     }
   }
 };
+
+template <typename T>
+void Engine<T>::split_preconditioned(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx,
+                                     void* iso, long long s_iso, int mode, double tol, int max_bond,
+                                     bool check_active, bool accumulate, void* work, long long s_work) {
+  // M_ = theta (mode 0) or theta^H (mode 1), l x k.  M_ = Q1 R1, R1 = L Q2 (QR of R1^H);
+  // one-sided Jacobi on L's columns gives U_L, and U_M = Q1 U_L is the isometry.
+  T* base = static_cast<T*>(pre_buf);
+  T* Qb = base;
+  T* R1h = base + pre_cap;
+  T* Lb = base + 2 * pre_cap;
+  T* Ub = base + 3 * pre_cap;
+  const long long sp = 4 * pre_cap;
+  const DimExpr Lr = mode == 0 ? M : N;  // column length l
+  const DimExpr Kc = mode == 0 ? N : M;  // number of columns k
+  const DimExpr R0 = dbond(pre_slot);
+  const int lu = ub(Lr), ku = ub(Kc);
+  const ChainState* stp = check_active ? d_state : nullptr;
+  {
+    ProfScope ps(ctx, TTG_PROF_QR, 0.0);
+    CK(qr_precondition<T>(theta, s_theta, M, N, mode, d_bonds, ld, pre_slot, Qb, sp, R1h, sp, lu, ku, stp, B, st));
+    CK(qr_precondition<T>(R1h, sp, Kc, R0, 0, d_bonds, ld, pre_slot, nullptr, 0, Lb, sp, ku, std::min(lu, ku), stp, B,
+                          st));
+  }
+  ctx->launches += 2;
+  S(Lb, sp, R0, R0, out_idx, Ub, sp, 0, tol, max_bond, check_active, accumulate, work, s_work, Warm(), true);
+  if (mode == 0)
+    G(Qb, sp, Ub, sp, iso, s_iso, M, dbond(out_idx), R0, OP_N, OP_N, check_active);
+  else
+    G(Ub, sp, Qb, sp, iso, s_iso, dbond(out_idx), N, R0, OP_C, OP_C, check_active);
+}
 
 // Host-side bookkeeping shared by simplify / canonicalize.
 struct Plan {
@@ -333,7 +398,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   const int L = target.n, B = target.count;
   cudaStream_t st = ctx->stream;
   Engine<T> E(ctx, L, B);
-  E.ld = L + 2;  // column L+1 is scratch (old bond during pass 3)
+  E.ld = L + 3;  // column L+1: old bond during pass 3; column L+2: preconditioner rank
   E.d = target.phys;
   E.t.assign(target.bonds.begin(), target.bonds.begin() + (L + 1));
   E.g.assign(guess.bonds.begin(), guess.bonds.begin() + (L + 1));
@@ -351,14 +416,16 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   const long long BIG = 1LL << 30;
   for (int k = 1; k <= L; ++k) dl[k] = std::min(BIG, dl[k - 1] * d[k - 1]);
   for (int k = L - 1; k >= 0; --k) dr[k] = std::min(BIG, dr[k + 1] * d[k]);
-  pb.assign(L + 2, 1);
-  bound.assign(L + 2, 1);
+  pb.assign(L + 3, 1);
+  bound.assign(L + 3, 1);
   for (int k = 0; k <= L; ++k) {
     pb[k] = (int)std::max(1LL, std::min({(long long)mb, dl[k], dr[k]}));
     bound[k] = std::max(q[k], pb[k]);
   }
   pb[0] = pb[L] = bound[0] = bound[L] = 1;
   bound[L + 1] = *std::max_element(bound.begin(), bound.end());
+  bound[L + 2] = 1;
+  for (int k = 0; k < L; ++k) bound[L + 2] = std::max({bound[L + 2], d[k] * bound[k], d[k] * bound[k + 1], q[k]});
 
   Plan P;
   P.psi_cap.resize(L);
@@ -383,10 +450,10 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     P.bcap = std::max(P.bcap, (long long)bound[k + 1] * bound[k + 1]);
     // R->L pass panels: theta = q_k x d p_{k+1}
     const long long l1 = (long long)d[k] * bound[k + 1], k1 = q[k];
-    if (!jacobi_svd_panel_in_smem(l1, k1, sizeof(T))) P.svd_work = std::max(P.svd_work, l1 * k1);
+    if (!jacobi_svd_panel_in_smem(l1, k1, sizeof(T))) P.svd_work = std::max(P.svd_work, (l1 + 1) * k1);
     // pass 3 (centre > 0): left unfolding (bound_k d) x bound_{k+1}
     const long long l3 = (long long)bound[k] * d[k], k3 = bound[k + 1];
-    if (!jacobi_svd_panel_in_smem(l3, k3, sizeof(T))) P.svd_work = std::max(P.svd_work, l3 * k3);
+    if (!jacobi_svd_panel_in_smem(l3, k3, sizeof(T))) P.svd_work = std::max(P.svd_work, (l3 + 1) * (k3 + 1));
   }
   for (int n = 0; n + 1 < L; ++n) {
     const long long dn = d[n], dn1 = d[n + 1];
@@ -396,9 +463,17 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     P.th = std::max(P.th, (long long)pb[n] * dn * dn1 * pb[n + 2]);
     const long long l = (long long)bound[n] * dn, kk = (long long)dn1 * bound[n + 2];
     if (!jacobi_svd_panel_in_smem(l, kk, sizeof(T)) || !jacobi_svd_panel_in_smem(kk, l, sizeof(T)))
-      P.svd_work = std::max(P.svd_work, l * kk);
+      P.svd_work = std::max(P.svd_work, (l + 1) * (kk + 1));
   }
   if (L >= 1) P.xz = std::max(P.xz, (long long)t[L - 1] * d[L - 1] * pb[L]);
+  // largest split panel (either orientation) for the grid-cooperative SVD workspace
+  long long svd_l = 1, svd_k = 1;
+  for (int k = 0; k < L; ++k) {
+    svd_l = std::max({svd_l, (long long)d[k] * bound[k + 1], (long long)bound[k] * d[k]});
+    svd_k = std::max({svd_k, (long long)q[k], (long long)bound[k + 1], (long long)d[k] * bound[k + 1],
+                      (long long)bound[k] * d[k]});
+  }
+  const long long svd_lk = std::max(svd_l, svd_k);
   P.env_cap.resize(L + 1);
   for (int k = 0; k <= L; ++k) P.env_cap[k] = (long long)pb[k] * t[k];
 
@@ -406,14 +481,14 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   ttg_dmps* psi = new_dmps(L, target.dtype, B, d, P.psi_cap, st);
   std::unique_ptr<ttg_dmps> psi_guard(psi);
   const size_t es = sizeof(T);
-  DevBuf bonds_buf((size_t)B * (L + 2) * sizeof(int), st);
+  DevBuf bonds_buf((size_t)B * (L + 3) * sizeof(int), st);
   DevBuf state_buf((size_t)B * sizeof(ChainState), st);
   E.d_bonds = bonds_buf.as<int>();
   E.d_state = state_buf.as<ChainState>();
   {
-    std::vector<int> hb((size_t)B * (L + 2));
+    std::vector<int> hb((size_t)B * (L + 3));
     for (int c = 0; c < B; ++c)
-      for (int k = 0; k <= L + 1; ++k) hb[(size_t)c * (L + 2) + k] = k <= L ? q[k] : 1;
+      for (int k = 0; k <= L + 2; ++k) hb[(size_t)c * (L + 3) + k] = k <= L ? q[k] : 1;
     CK(cudaMemcpyAsync(E.d_bonds, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));  // hb goes out of scope
   }
@@ -428,6 +503,12 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
       qbW2(any_blocked ? (size_t)B * P.qb_W * es : 0, st), qbP(any_blocked ? (size_t)B * P.qb_P * es : 0, st);
   const QrBlockedWork qbw{qbA.p, qbV.p, qbT.p, qbW1.p, qbW2.p, qbP.p, P.qb_A, P.qb_V, P.qb_T, P.qb_W, P.qb_P};
   DevBuf svdw(P.svd_work ? (size_t)B * P.svd_work * es : 0, st);
+  DevBuf svdg(B <= 16 ? (size_t)B * jacobi_grid_work_bytes((int)svd_lk, (int)svd_lk, es) : 0, st);
+  E.svd_grid_work = B <= 16 ? svdg.p : nullptr;
+  E.pre_cap = svd_lk * svd_lk;
+  DevBuf prebuf((size_t)B * 4 * E.pre_cap * es, st);
+  E.pre_buf = prebuf.p;
+  E.pre_slot = L + 2;
   const long long sC = P.ccap, sR = P.rcap, sBb = P.bcap;
   T* cbuf[2] = {C0.as<T>(), C1.as<T>()};
   const double tol = s.tolerance;
@@ -504,6 +585,22 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     }
   }
 
+  // warm-start frames per two-site block n: U (after L->R) and V (after R->L)
+  DevBuf TH2(variational ? (size_t)B * P.th * es : 0, st);
+  std::vector<long long> fcap(L, 1);
+  std::vector<DevBuf> frameU, frameV;
+  frameU.reserve(L);
+  frameV.reserve(L);
+  for (int n = 0; n + 1 < L; ++n) {
+    const long long side = std::max((long long)bound[n] * d[n], (long long)d[n + 1] * bound[n + 2]);
+    fcap[n] = side * side;
+    frameU.emplace_back((size_t)B * fcap[n] * es, st);
+    frameV.emplace_back((size_t)B * fcap[n] * es, st);
+  }
+  DevBuf fmeta((size_t)2 * B * L * sizeof(int), st);
+  CK(cudaMemsetAsync(fmeta.p, 0, (size_t)2 * B * L * sizeof(int), st));
+  int* fU = fmeta.as<int>();
+  int* fV = fU + (size_t)B * L;
   // ---- pass 2: truncating right-to-left sweep (mps.hpp:206-210, 253-265)
   for (int k = L - 1; k >= 1; --k) {
     const DimExpr rows = dconst(q[k]);
@@ -554,22 +651,6 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     }
     DevBuf XZ((size_t)B * P.xz * es, st), YW((size_t)B * P.yw * es, st), TH((size_t)B * P.th * es, st);
     const long long sxz = P.xz, syw = P.yw, sth = P.th;
-    // warm-start frames per two-site block n: U (after L->R) and V (after R->L)
-    DevBuf TH2((size_t)B * P.th * es, st);
-    std::vector<long long> fcap(L, 1);
-    std::vector<DevBuf> frameU, frameV;
-    frameU.reserve(L);
-    frameV.reserve(L);
-    for (int n = 0; n + 1 < L; ++n) {
-      const long long side = std::max((long long)bound[n] * d[n], (long long)d[n + 1] * bound[n + 2]);
-      fcap[n] = side * side;
-      frameU.emplace_back((size_t)B * fcap[n] * es, st);
-      frameV.emplace_back((size_t)B * fcap[n] * es, st);
-    }
-    DevBuf fmeta((size_t)2 * B * L * sizeof(int), st);
-    CK(cudaMemsetAsync(fmeta.p, 0, (size_t)2 * B * L * sizeof(int), st));
-    int* fU = fmeta.as<int>();
-    int* fV = fU + (size_t)B * L;
     CK(fill_one<T>(lenv[0].as<T>(), P.env_cap[0], B, st));
     CK(fill_one<T>(renv[L].as<T>(), P.env_cap[L], B, st));
     ctx->launches += 2;
@@ -583,8 +664,20 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
           OP_R, OP_T, false);
     }
     CK(begin_sweeps(E.d_state, B, st));
+    // from here on psi bonds are <= pb (truncated canonical form): tighter launch bounds
+    for (int k = 0; k <= L; ++k) bound[k] = pb[k];
+    bound[L + 1] = *std::max_element(pb.begin(), pb.begin() + L + 1);
+    bound[L + 2] = 1;
+    for (int k = 0; k < L; ++k) bound[L + 2] = std::max({bound[L + 2], d[k] * pb[k], d[k] * pb[k + 1]});
     ++ctx->launches;
 
+    // Frames of the previous split at a bond as a warm start: off by default (for
+    // graded spectra a slightly stale frame does not cut the Jacobi sweeps; the
+    // QR preconditioner does), TTG_SVD_WARM=1 enables it.
+    static const bool warm_frames = [] {
+      const char* e = getenv("TTG_SVD_WARM");
+      return e && e[0] == '1';
+    }();
     // ---- sweeps (simplify.hpp:66-91, 114-125)
     const int nsweeps = std::max(1, s.max_sweeps);
     std::vector<ChainState> hstate(B);
@@ -597,16 +690,17 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
             OP_N, OP_N, true);
         E.G(YW.p, syw, renv[n + 2].p, P.env_cap[n + 2], TH.p, sth, dbond(n, dn * dn1), dbond(n + 2),
             dconst(t[n + 2]), OP_N, OP_T, true);
-        // warm start: theta V_prev (same singular values, same U)
-        E.G(TH.p, sth, frameV[n].p, fcap[n], TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n + 2, dn1), OP_N,
-            OP_N, true);
+        // optional warm start: theta V_prev (same singular values, same U)
         typename Engine<T>::Warm wl;
-        wl.pre = TH2.p;
+        if (warm_frames)
+          E.G(TH.p, sth, frameV[n].p, fcap[n], TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n + 2, dn1), OP_N,
+              OP_N, true);
+        wl.pre = warm_frames ? TH2.p : nullptr;
         wl.s_pre = sth;
-        wl.fin = fV + n;
-        wl.fout = fU + n;
+        wl.fin = warm_frames ? fV + n : nullptr;
+        wl.fout = warm_frames ? fU + n : nullptr;
         wl.fld = L;
-        wl.frame = frameU[n].p;
+        wl.frame = warm_frames ? frameU[n].p : nullptr;
         wl.s_frame = fcap[n];
         E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n], P.psi_cap[n], 0, tol, mb, true, false,
             svdw.p, P.svd_work, wl);
@@ -623,16 +717,17 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
             true);
         E.G(lenv[n].p, P.env_cap[n], YW.p, syw, TH.p, sth, dbond(n), dbond(n + 2, dn * dn1), dconst(t[n]), OP_N,
             OP_N, true);
-        // warm start: U_prev^H theta (same singular values, same V)
-        E.G(frameU[n].p, fcap[n], TH.p, sth, TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n, dn), OP_C, OP_N,
-            true);
+        // optional warm start: U_prev^H theta (same singular values, same V)
         typename Engine<T>::Warm wr;
-        wr.pre = TH2.p;
+        if (warm_frames)
+          E.G(frameU[n].p, fcap[n], TH.p, sth, TH2.p, sth, dbond(n, dn), dbond(n + 2, dn1), dbond(n, dn), OP_C, OP_N,
+              true);
+        wr.pre = warm_frames ? TH2.p : nullptr;
         wr.s_pre = sth;
-        wr.fin = fU + n;
-        wr.fout = fV + n;
+        wr.fin = warm_frames ? fU + n : nullptr;
+        wr.fout = warm_frames ? fV + n : nullptr;
         wr.fld = L;
-        wr.frame = frameV[n].p;
+        wr.frame = warm_frames ? frameV[n].p : nullptr;
         wr.s_frame = fcap[n];
         E.S(TH.p, sth, dbond(n, dn), dbond(n + 2, dn1), n + 1, psi->site[n + 1], P.psi_cap[n + 1], 1, tol, mb, true,
             false, svdw.p, P.svd_work, wr);
@@ -662,11 +757,11 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   DevBuf norms((size_t)B * sizeof(double), st);
   {
     // centre = out_center; its shape is p_c x d x p_{c+1}
-    std::vector<int> hb((size_t)B * (L + 2));
+    std::vector<int> hb((size_t)B * (L + 3));
     CK(cudaMemcpyAsync(hb.data(), E.d_bonds, hb.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int c = 0; c < B; ++c)
-      for (int k = 0; k <= L; ++k) psi->bonds[(size_t)c * (L + 1) + k] = hb[(size_t)c * (L + 2) + k];
+      for (int k = 0; k <= L; ++k) psi->bonds[(size_t)c * (L + 1) + k] = hb[(size_t)c * (L + 3) + k];
   }
   const int cc = out_center;
   CK(frob2<T>(static_cast<T*>(psi->site[cc]), P.psi_cap[cc], dbond(cc, d[cc]), dbond(cc + 1), E.d_bonds, E.ld,

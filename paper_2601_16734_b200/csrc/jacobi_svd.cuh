@@ -49,10 +49,20 @@ struct SvdParams {
 constexpr size_t SVD_SMEM_LIMIT = 220 * 1024;
 inline size_t jacobi_svd_meta_bytes(long long kmax) { return (size_t)kmax * (2 * sizeof(double) + sizeof(int)) + 16; }
 inline bool jacobi_svd_panel_in_smem(long long lmax, long long kmax, size_t es) {
-  return jacobi_svd_meta_bytes(kmax) + (size_t)lmax * kmax * es <= SVD_SMEM_LIMIT;
+  return jacobi_svd_meta_bytes(kmax) + (size_t)(lmax | 1) * kmax * es <= SVD_SMEM_LIMIT;
 }
 
 template <typename T>
 cudaError_t jacobi_svd(const SvdParams& p, int lmax, int kmax, int chains, cudaStream_t s);
+
+// Grid-cooperative variant for a few large splits: the columns are grouped in
+// blocks, every CTA of a cooperative grid owns one block pair per block round
+// (its whole CTA works on the pair: rows split over threads, one cross-warp
+// reduction per sub-round), and rounds are separated by grid-wide barriers.
+// `work` must hold, per chain, jacobi_grid_work_bytes(lmax, kmax) bytes.
+size_t jacobi_grid_work_bytes(int lmax, int kmax, size_t es);
+bool jacobi_grid_eligible(int lmax, int kmax, int chains, size_t es);
+template <typename T>
+cudaError_t jacobi_svd_grid(const SvdParams& p, int lmax, int kmax, int chains, void* work, cudaStream_t s);
 
 }  // namespace ttg

@@ -171,7 +171,275 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(QrParams p, int in_smem)
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(QR_THREADS) qr_r_kernel(const T* A, long long sA, DimExpr M, DimExpr N, int* bonds,
+                                                           int ld, int out_idx, T* R, long long sR) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[33];
+  __shared__ T s_tau;
+  const int chain = blockIdx.x;
+  const int m = M.eval(bonds, chain, ld), n = N.eval(bonds, chain, ld);
+  A += sA * chain;
+  R += sR * chain;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (m <= n) {
+    for (int idx = tid; idx < m * n; idx += blockDim.x) R[idx] = A[idx];
+    if (tid == 0) bonds[chain * ld + out_idx] = m;
+    return;
+  }
+  T* Wk = reinterpret_cast<T*>(smem_raw);
+  for (int idx = tid; idx < m * n; idx += blockDim.x) {
+    const int i = idx / n, c = idx % n;
+    Wk[c * m + i] = A[idx];
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    T* v = Wk + j * m;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < m; i += blockDim.x) part += abs2(v[i]);
+    const double xn2 = block_sum(part, red);
+    if (tid == 0) {
+      const T alpha = v[j];
+      double ar, ai;
+      if constexpr (Scalar<T>::is_complex) {
+        ar = alpha.x;
+        ai = alpha.y;
+      } else {
+        ar = alpha;
+        ai = 0.0;
+      }
+      T t = Scalar<T>::zero();
+      red[0] = 1.0;
+      red[1] = 0.0;
+      if (!(xn2 == 0.0 && ai == 0.0)) {
+        const double beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        if constexpr (Scalar<T>::is_complex) {
+          t = cplx{(beta - ar) / beta, -ai / beta};
+          const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+          red[0] = dr / den;
+          red[1] = -di / den;
+          v[j] = cplx{beta, 0.0};
+        } else {
+          t = (beta - ar) / beta;
+          red[0] = 1.0 / (ar - beta);
+          v[j] = beta;
+        }
+      }
+      s_tau = t;
+    }
+    __syncthreads();
+    T sc;
+    if constexpr (Scalar<T>::is_complex)
+      sc = cplx{red[0], red[1]};
+    else
+      sc = red[0];
+    for (int i = j + 1 + tid; i < m; i += blockDim.x) v[i] = mul(v[i], sc);
+    __syncthreads();
+    const T ct = conj_(s_tau);
+    for (int c = j + 1 + warp; c < n; c += nwarps) {
+      T* a = Wk + c * m;
+      T w = Scalar<T>::zero();
+      for (int i = j + lane; i < m; i += 32) w = add(w, cmul(i == j ? Scalar<T>::one() : v[i], a[i]));
+      if constexpr (Scalar<T>::is_complex) {
+        w.x = warp_sum(w.x);
+        w.y = warp_sum(w.y);
+      } else {
+        w = warp_sum(w);
+      }
+      const T f = mul(ct, w);
+      for (int i = j + lane; i < m; i += 32) a[i] = sub(a[i], mul(i == j ? Scalar<T>::one() : v[i], f));
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx / n, c = idx % n;
+    R[idx] = (c >= i) ? Wk[c * m + i] : Scalar<T>::zero();
+  }
+  if (tid == 0) bonds[chain * ld + out_idx] = n;
+}
+
+// a_c[j:] -= f v (v^H a_c[j:]) for the columns c in [c0, c1) handled by this
+// warp, four at a time so that the four reductions overlap.
+template <typename T>
+__device__ __forceinline__ void apply_reflector_cols(T* Wk, int l, int lw, const T* v, int j, T f_scale, int c0,
+                                                     int c1, int warp, int nwarps, int lane) {
+  for (int cb = c0 + warp; cb < c1; cb += 4 * nwarps) {
+    T w[4];
+    T* a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = cb + u * nwarps;
+      a[u] = Wk + (c < c1 ? c : c0) * lw;
+      w[u] = Scalar<T>::zero();
+    }
+    for (int i = j + lane; i < l; i += 32) {
+      const T vi = (i == j) ? Scalar<T>::one() : v[i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = add(w[u], cmul(vi, a[u][i]));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if constexpr (Scalar<T>::is_complex) {
+        w[u].x = warp_sum(w[u].x);
+        w[u].y = warp_sum(w[u].y);
+      } else {
+        w[u] = warp_sum(w[u]);
+      }
+      w[u] = mul(f_scale, w[u]);
+    }
+    for (int i = j + lane; i < l; i += 32) {
+      const T vi = (i == j) ? Scalar<T>::one() : v[i];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (cb + u * nwarps < c1) a[u][i] = sub(a[u][i], mul(vi, w[u]));
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(QR_THREADS) qr_pre_kernel(const T* A, long long sA, DimExpr Md, DimExpr Nd, int trans,
+                                                             int* bonds, int ld, int out_idx, T* Q, long long sQ,
+                                                             T* RH, long long sRH, const ChainState* st) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ T s_tau;
+  __shared__ T taus[1024];
+  const int chain = blockIdx.x;
+  if (st && !st[chain].active) return;
+  const int mi = Md.eval(bonds, chain, ld), ni = Nd.eval(bonds, chain, ld);
+  const int l = trans ? ni : mi, k = trans ? mi : ni, r0 = min(l, k);
+  const int lw = l | 1;  // odd column stride: transposing loads/stores are bank-conflict free
+  A += sA * chain;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  T* Wk = reinterpret_cast<T*>(smem_raw);
+  // W[c*l + i] = M[i, c]
+  for (int idx = tid; idx < mi * ni; idx += blockDim.x) {
+    const int r = idx / ni, c = idx % ni;
+    if (trans)
+      Wk[r * lw + c] = conj_(A[idx]);
+    else
+      Wk[c * lw + r] = A[idx];
+  }
+  __syncthreads();
+  // Column j: warp 0 forms the reflector (norm, beta, tau, scaling of v) without
+  // a block-wide reduction; one barrier publishes it, all warps update the
+  // trailing columns, one barrier closes the step.
+  for (int j = 0; j < r0; ++j) {
+    T* v = Wk + j * lw;
+    if (warp == 0) {
+      double part = 0.0;
+      for (int i = j + 1 + lane; i < l; i += 32) part += abs2(v[i]);
+      const double xn2 = warp_sum(part);
+      const T alpha = v[j];
+      double ar, ai;
+      if constexpr (Scalar<T>::is_complex) {
+        ar = alpha.x;
+        ai = alpha.y;
+      } else {
+        ar = alpha;
+        ai = 0.0;
+      }
+      T t = Scalar<T>::zero();
+      T sc = Scalar<T>::one();
+      double beta = ar;
+      const bool refl = !(xn2 == 0.0 && ai == 0.0);
+      if (refl) {
+        beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        if constexpr (Scalar<T>::is_complex) {
+          t = cplx{(beta - ar) / beta, -ai / beta};
+          const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+          sc = cplx{dr / den, -di / den};
+        } else {
+          t = (beta - ar) / beta;
+          sc = 1.0 / (ar - beta);
+        }
+      }
+      for (int i = j + 1 + lane; i < l; i += 32) v[i] = mul(v[i], sc);
+      if (lane == 0) {
+        if (refl) {
+          if constexpr (Scalar<T>::is_complex)
+            v[j] = cplx{beta, 0.0};
+          else
+            v[j] = beta;
+        }
+        s_tau = t;
+        taus[j] = t;
+      }
+    }
+    __syncthreads();
+    apply_reflector_cols<T>(Wk, l, lw, v, j, conj_(s_tau), j + 1, k, warp, nwarps, lane);
+    __syncthreads();
+  }
+  // R1^H (k x r0): RH[c, i] = conj(R1[i, c]) for c >= i
+  T* rh = RH + sRH * chain;
+  for (int idx = tid; idx < k * r0; idx += blockDim.x) {
+    const int c = idx / r0, i = idx % r0;
+    rh[idx] = (c >= i) ? conj_(Wk[c * lw + i]) : Scalar<T>::zero();
+  }
+  if (tid == 0) bonds[chain * ld + out_idx] = r0;
+  if (!Q) return;
+  __syncthreads();
+  // Q1 in place over the reflectors (xORG2R), columns 0..r0-1
+  for (int j = r0 - 1; j >= 0; --j) {
+    T* v = Wk + j * lw;
+    const T tj = taus[j];
+    apply_reflector_cols<T>(Wk, l, lw, v, j, tj, j + 1, r0, warp, nwarps, lane);  // (xORG2R)
+    __syncthreads();
+    for (int i = tid; i < l; i += blockDim.x) {
+      if (i < j)
+        v[i] = Scalar<T>::zero();
+      else if (i == j)
+        v[i] = sub(Scalar<T>::one(), tj);
+      else
+        v[i] = mul(sub(Scalar<T>::zero(), tj), v[i]);
+    }
+    __syncthreads();
+  }
+  T* q = Q + sQ * chain;
+  for (int idx = tid; idx < l * r0; idx += blockDim.x) {
+    const int i = idx / r0, c = idx % r0;
+    q[idx] = Wk[c * lw + i];
+  }
+}
+
 }  // namespace
+
+template <typename T>
+cudaError_t qr_precondition(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
+                            int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
+                            const ChainState* st, int chains, cudaStream_t s) {
+  const size_t bytes = (size_t)(lmax | 1) * kmax * sizeof(T);
+  if (bytes > QR_R_SMEM_LIMIT || (lmax < kmax ? lmax : kmax) > 1024) return cudaErrorInvalidValue;
+  cudaError_t e =
+      cudaFuncSetAttribute(qr_pre_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_R_SMEM_LIMIT);
+  if (e != cudaSuccess) return e;
+  qr_pre_kernel<T><<<chains, QR_THREADS, bytes, s>>>(static_cast<const T*>(A), sA, M, N, trans, bonds, ld, out_idx,
+                                                    static_cast<T*>(Q), sQ, static_cast<T*>(RH), sRH, st);
+  return cudaGetLastError();
+}
+
+template cudaError_t qr_precondition<double>(const void*, long long, DimExpr, DimExpr, int, int*, int, int, void*,
+                                             long long, void*, long long, int, int, const ChainState*, int,
+                                             cudaStream_t);
+template cudaError_t qr_precondition<cplx>(const void*, long long, DimExpr, DimExpr, int, int*, int, int, void*,
+                                           long long, void*, long long, int, int, const ChainState*, int,
+                                           cudaStream_t);
+
+template <typename T>
+cudaError_t qr_r_factor(const void* A, long long sA, DimExpr M, DimExpr N, int* bonds, int ld, int out_idx, void* R,
+                        long long sR, int mmax, int nmax, int chains, cudaStream_t s) {
+  const size_t bytes = (size_t)mmax * nmax * sizeof(T);
+  if (bytes > QR_R_SMEM_LIMIT) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(qr_r_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_R_SMEM_LIMIT);
+  if (e != cudaSuccess) return e;
+  qr_r_kernel<T><<<chains, QR_THREADS, bytes, s>>>(static_cast<const T*>(A), sA, M, N, bonds, ld, out_idx,
+                                                  static_cast<T*>(R), sR);
+  return cudaGetLastError();
+}
+
+template cudaError_t qr_r_factor<double>(const void*, long long, DimExpr, DimExpr, int*, int, int, void*, long long,
+                                         int, int, int, cudaStream_t);
+template cudaError_t qr_r_factor<cplx>(const void*, long long, DimExpr, DimExpr, int*, int, int, void*, long long,
+                                       int, int, int, cudaStream_t);
 
 template <typename T>
 size_t qr_workspace_elems(int m, int n) {

@@ -18,6 +18,28 @@ struct QrParams {
 };
 
 template <typename T> size_t qr_workspace_elems(int m, int n);
+
+// R factor only, shapes read from the device bond table: for a tall m x n
+// panel (m > n) writes the n x n upper-triangular R (the right singular vectors
+// and singular values of A are those of R); otherwise copies A.  The effective
+// row count (min(m, n)) is written to bonds[c*ld + out_idx].  One CTA per chain,
+// panel in shared memory (bytes <= qr_r_smem_limit).
+constexpr size_t QR_R_SMEM_LIMIT = 200 * 1024;  // + up to 16 KB static (reflector scalars)
+// Preconditioner of the truncated split (Drmac-Veselic style): for the
+// l x k matrix M = A (trans = 0) or A^H (trans = 1) compute M = Q1 R1 with
+// r0 = min(l, k) and write Q1 (l x r0, row-major, nullable) and R1^H
+// (k x r0, row-major); r0 goes to bonds[c*ld + out_idx].  Applied twice
+// (the second time to R1^H without Q) it yields L = R2^H with
+// M = Q1 L Q2, on which one-sided Jacobi needs a few sweeps instead of tens
+// for the graded spectra of MPS splits.  Shared memory holds l*k elements.
+template <typename T>
+cudaError_t qr_precondition(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
+                            int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
+                            const ChainState* st, int chains, cudaStream_t s);
+
+template <typename T>
+cudaError_t qr_r_factor(const void* A, long long sA, DimExpr M, DimExpr N, int* bonds, int ld, int out_idx, void* R,
+                        long long sR, int mmax, int nmax, int chains, cudaStream_t s);
 template <typename T> cudaError_t householder_qr(const QrParams& p, int chains, cudaStream_t s);
 
 }  // namespace ttg

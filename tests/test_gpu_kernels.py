@@ -103,10 +103,17 @@ def _svd(theta, mode, tol=0.0, max_bond=0):
     return iso, sv, r, e2.value
 
 
+@pytest.fixture(params=["cta", "grid"])
+def svd_impl(request, monkeypatch):
+    monkeypatch.setenv("TTG_DEBUG_SVD_GRID", "1" if request.param == "grid" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("dtype", [np.float64, np.complex128])
-@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (4, 4), (6, 4), (4, 6), (32, 32), (128, 128), (64, 150), (192, 128)])
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (4, 4), (6, 4), (4, 6), (32, 32), (128, 128), (64, 150), (192, 128),
+                                   (300, 260)])
 @pytest.mark.parametrize("mode", [0, 1])
-def test_jacobi_svd_random(dtype, shape, mode):
+def test_jacobi_svd_random(dtype, shape, mode, svd_impl):
     m, n = shape
     rng = np.random.default_rng(m * 7 + n)
     th = rng.standard_normal((m, n))
@@ -135,7 +142,7 @@ def test_svd_kat_identity():
     assert r == 1 and abs(np.sqrt(e2) - 1 / np.sqrt(2)) < 1e-15
 
 
-def test_svd_truncation_rule():
+def test_svd_truncation_rule(svd_impl):
     """schmidt.hpp:40-59: strict > tol*s0, at least 1, at most max_bond; err = sqrt(sum dropped^2)."""
     rng = np.random.default_rng(3)
     U, _ = np.linalg.qr(rng.standard_normal((10, 10)))
@@ -152,7 +159,7 @@ def test_svd_truncation_rule():
     assert r == 1
 
 
-def test_svd_rank_deficient_drops_zero_values():
+def test_svd_rank_deficient_drops_zero_values(svd_impl):
     rng = np.random.default_rng(11)
     th = rng.standard_normal((64, 5)) @ rng.standard_normal((5, 64))
     _, sv, r, _ = _svd(th, 0, tol=1e-12)
