@@ -266,6 +266,10 @@ struct Engine {
     long long s_frame = 0;
   };
 
+  void split_large(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso,
+                   long long s_iso, int mode, double tol, int max_bond, bool check_active, bool accumulate,
+                   void* work, long long s_work);
+
   void split_preconditioned(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso,
                             long long s_iso, int mode, double tol, int max_bond, bool check_active, bool accumulate,
                             void* work, long long s_work);
@@ -306,6 +310,12 @@ struct Engine {
       return !(e && e[0] == '0');
     }();
     const bool grid_path = svd_grid_work && jacobi_grid_eligible(mode == 0 ? mu : nu, mode == 0 ? nu : mu, B, sizeof(T));
+    if (!no_pre && pre_ok && B == 1 && w.pre == nullptr && std::min(mu, nu) >= 24 &&
+        (std::max(mu, nu) > 160 || (size_t)(std::max(mu, nu) | 1) * std::max(mu, nu) * sizeof(T) > QR_R_SMEM_LIMIT)) {
+      split_large(theta, s_theta, M, N, out_idx, iso, s_iso, mode, tol, max_bond, check_active, accumulate, work,
+                  s_work);
+      return;
+    }
     if (!no_pre && pre_ok && pre_buf && !grid_path && w.pre == nullptr && (long long)mu * nu >= 24 * 24 &&
         (size_t)(std::max(mu, nu) | 1) * std::max(mu, nu) * sizeof(T) <= QR_R_SMEM_LIMIT && std::min(mu, nu) <= 1024 &&
         (long long)std::max(mu, nu) * std::max(mu, nu) <= pre_cap) {
@@ -381,6 +391,58 @@ void Engine<T>::split_preconditioned(const void* theta, long long s_theta, DimEx
     G(Qb, sp, Ub, sp, iso, s_iso, M, dbond(out_idx), R0, OP_N, OP_N, check_active);
   else
     G(Ub, sp, Qb, sp, iso, s_iso, dbond(out_idx), N, R0, OP_C, OP_C, check_active);
+}
+
+// Large split of a single chain: shapes are read back from the device (one sync;
+// each such split is milliseconds of work), M_ = theta or theta^H is reduced by
+// two blocked Householder QRs (M_ = Q1 R1, R1^H = Q2 R2, so M_ = Q1 R2^H Q2^H)
+// and one-sided Jacobi runs on the square R2 (mode 1 orthogonalises the
+// columns of R2^H = L).  Isometry: U_M = Q1 U_L.
+template <typename T>
+void Engine<T>::split_large(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso,
+                            long long s_iso, int mode, double tol, int max_bond, bool check_active, bool accumulate,
+                            void* work, long long s_work) {
+  (void)s_theta;
+  (void)s_iso;
+  std::vector<int> hb(ld);
+  ChainState hs{};
+  CK(cudaMemcpyAsync(hb.data(), d_bonds, ld * sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (check_active) CK(cudaMemcpyAsync(&hs, d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (check_active && !hs.active) return;
+  const int m = M.eval(hb.data(), 0, ld), n = N.eval(hb.data(), 0, ld);
+  const int l = mode == 0 ? m : n, k = mode == 0 ? n : m, r0 = std::min(l, k);
+  const size_t es = sizeof(T);
+  DevBuf Mb((size_t)l * k * es, st), Q1((size_t)l * r0 * es, st), R1((size_t)r0 * k * es, st),
+      R1h((size_t)k * r0 * es, st), R2((size_t)r0 * r0 * es, st), Ut((size_t)r0 * r0 * es, st);
+  if (mode == 0)
+    CK(cudaMemcpyAsync(Mb.p, theta, (size_t)m * n * es, cudaMemcpyDeviceToDevice, st));
+  else
+    CK(conj_transpose<T>(theta, 0, m, n, Mb.p, 0, 1, st));
+  ++ctx->launches;
+  auto blocked = [&](void* A, int rows, int cols, void* Q, void* R) {
+    size_t a, v, t2, w2, pp;
+    qr_blocked_elems<T>(rows, cols, &a, &v, &t2, &w2, &pp);
+    DevBuf wa(a * es, st), wv(v * es, st), wt(t2 * es, st), w1b(w2 * es, st), w2b(w2 * es, st), wp(pp * es, st);
+    QrParams qp{A, 0, Q, 0, R, 0, nullptr, 0, rows, cols};
+    const QrBlockedWork qw{wa.p, wv.p, wt.p, w1b.p, w2b.p, wp.p, 0, 0, 0, 0, 0};
+    long long nl = 0;
+    const double big = std::max(rows, cols), sm = std::min(rows, cols);
+    ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * (Q ? 4.0 : 2.0) * sm * sm * (big - sm / 3.0));
+    CK(householder_qr_blocked<T>(qp, qw, 1, st, &nl));
+    ctx->launches += nl;
+  };
+  blocked(Mb.p, l, k, Q1.p, R1.p);
+  CK(conj_transpose<T>(R1.p, 0, r0, k, R1h.p, 0, 1, st));
+  ++ctx->launches;
+  blocked(R1h.p, k, r0, nullptr, R2.p);
+  // Jacobi (mode 1) on R2: iso_tmp = U_L^H (r x r0), rank -> bonds[out_idx]
+  S(R2.p, 0, dconst(r0), dconst(r0), out_idx, Ut.p, 0, 1, tol, max_bond, check_active, accumulate, work, s_work, Warm(),
+    true);
+  if (mode == 0)  // psi_n = Q1 U_L = Q1 (U_L^H)^H  (m x r)
+    G(Q1.p, 0, Ut.p, 0, iso, 0, dconst(m), dbond(out_idx), dconst(r0), OP_N, OP_C, check_active);
+  else  // psi_{n+1} = (Q1 U_L)^H = U_L^H Q1^H  (r x n)
+    G(Ut.p, 0, Q1.p, 0, iso, 0, dbond(out_idx), dconst(n), dconst(r0), OP_N, OP_C, check_active);
 }
 
 // Host-side bookkeeping shared by simplify / canonicalize.
@@ -505,7 +567,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   DevBuf svdw(P.svd_work ? (size_t)B * P.svd_work * es : 0, st);
   DevBuf svdg(B <= 16 ? (size_t)B * jacobi_grid_work_bytes((int)svd_lk, (int)svd_lk, es) : 0, st);
   E.svd_grid_work = B <= 16 ? svdg.p : nullptr;
-  E.pre_cap = svd_lk * svd_lk;
+  E.pre_cap = std::min(svd_lk, 256LL) * std::min(svd_lk, 256LL);  // small preconditioned splits only
   DevBuf prebuf((size_t)B * 4 * E.pre_cap * es, st);
   E.pre_buf = prebuf.p;
   E.pre_slot = L + 2;
@@ -585,14 +647,21 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     }
   }
 
+  // Frames of the previous split at a bond as a warm start: off by default (for
+  // graded spectra a slightly stale frame does not cut the Jacobi sweeps; the
+  // QR preconditioner does), TTG_SVD_WARM=1 enables it.
+  static const bool warm_frames = [] {
+    const char* e = getenv("TTG_SVD_WARM");
+    return e && e[0] == '1';
+  }();
   // warm-start frames per two-site block n: U (after L->R) and V (after R->L)
-  DevBuf TH2(variational ? (size_t)B * P.th * es : 0, st);
+  DevBuf TH2(variational && warm_frames ? (size_t)B * P.th * es : 0, st);
   std::vector<long long> fcap(L, 1);
   std::vector<DevBuf> frameU, frameV;
   frameU.reserve(L);
   frameV.reserve(L);
   for (int n = 0; n + 1 < L; ++n) {
-    const long long side = std::max((long long)bound[n] * d[n], (long long)d[n + 1] * bound[n + 2]);
+    const long long side = std::max((long long)pb[n] * d[n], (long long)d[n + 1] * pb[n + 2]);
     fcap[n] = side * side;
     frameU.emplace_back((size_t)B * fcap[n] * es, st);
     frameV.emplace_back((size_t)B * fcap[n] * es, st);
@@ -671,13 +740,6 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     for (int k = 0; k < L; ++k) bound[L + 2] = std::max({bound[L + 2], d[k] * pb[k], d[k] * pb[k + 1]});
     ++ctx->launches;
 
-    // Frames of the previous split at a bond as a warm start: off by default (for
-    // graded spectra a slightly stale frame does not cut the Jacobi sweeps; the
-    // QR preconditioner does), TTG_SVD_WARM=1 enables it.
-    static const bool warm_frames = [] {
-      const char* e = getenv("TTG_SVD_WARM");
-      return e && e[0] == '1';
-    }();
     // ---- sweeps (simplify.hpp:66-91, 114-125)
     const int nsweeps = std::max(1, s.max_sweeps);
     std::vector<ChainState> hstate(B);

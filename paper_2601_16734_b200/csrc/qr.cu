@@ -606,6 +606,24 @@ __global__ void __launch_bounds__(PANEL_THREADS) qr_panel_kernel(T* A, long long
 }
 
 template <typename T>
+__global__ void conj_transpose_kernel(const T* src, long long s_src, int rows, int cols, T* dst, long long s_dst) {
+  __shared__ T tile[32][33];
+  const int chain = blockIdx.z;
+  src += s_src * chain;
+  dst += s_dst * chain;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int yy = threadIdx.y; yy < 32; yy += 8) {
+    const int r = by + yy, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[yy][threadIdx.x] = src[(size_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int yy = threadIdx.y; yy < 32; yy += 8) {
+    const int c = bx + yy, r = by + threadIdx.x;  // dst[c, r] = conj(src[r, c])
+    if (r < rows && c < cols) dst[(size_t)c * rows + r] = conj_(tile[threadIdx.x][yy]);
+  }
+}
+
+template <typename T>
 __global__ void copy_in_kernel(const T* src, long long s_src, T* dst, long long s_dst, long long n) {
   const int chain = blockIdx.y;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -709,6 +727,10 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   }
   upper_kernel<T><<<dim3(blocks_for((long long)k * n), chains), 256, 0, s>>>(A, w.sA, n, static_cast<T*>(p.R), p.sR, k);
   T* Q = static_cast<T*>(p.Q);
+  if (!Q) {  // R only
+    if (launches) *launches += nl + 1;
+    return cudaGetLastError();
+  }
   eye_kernel<T><<<dim3(blocks_for((long long)m * k), chains), 256, 0, s>>>(Q, p.sQ, m, k);
   nl += 2;
   const int nblk = (k + QR_NB - 1) / QR_NB;
@@ -742,6 +764,18 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   if (launches) *launches += nl;
   return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t conj_transpose(const void* src, long long s_src, int rows, int cols, void* dst, long long s_dst, int chains,
+                           cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || chains <= 0) return cudaSuccess;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, chains);
+  conj_transpose_kernel<T><<<grid, dim3(32, 8), 0, s>>>(static_cast<const T*>(src), s_src, rows, cols,
+                                                        static_cast<T*>(dst), s_dst);
+  return cudaGetLastError();
+}
+template cudaError_t conj_transpose<double>(const void*, long long, int, int, void*, long long, int, cudaStream_t);
+template cudaError_t conj_transpose<cplx>(const void*, long long, int, int, void*, long long, int, cudaStream_t);
 
 template size_t qr_blocked_elems<double>(int, int, size_t*, size_t*, size_t*, size_t*, size_t*);
 template size_t qr_blocked_elems<cplx>(int, int, size_t*, size_t*, size_t*, size_t*, size_t*);

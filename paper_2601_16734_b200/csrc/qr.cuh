@@ -62,6 +62,11 @@ struct QrBlockedWork {
 };
 constexpr int QR_NB = 32;
 template <typename T> size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t* sW, size_t* sP);
+// dst (cols x rows) = src^H (rows x cols), row-major, batched
+template <typename T>
+cudaError_t conj_transpose(const void* src, long long s_src, int rows, int cols, void* dst, long long s_dst, int chains,
+                           cudaStream_t s);
+// p.Q == nullptr: R only (no Q formation)
 template <typename T>
 cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, int chains, cudaStream_t s,
                                    long long* launches);
