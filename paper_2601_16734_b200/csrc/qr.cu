@@ -605,6 +605,177 @@ __global__ void __launch_bounds__(PANEL_THREADS) qr_panel_kernel(T* A, long long
   }
 }
 
+// Tall panels (not in shared memory): rows are spread over 1024 threads, the
+// panel lives column-major in an L2-resident scratch, and for every column all
+// trailing dot products are reduced together (one block reduction of <= 31
+// values per column instead of one per column pair).
+constexpr int PANEL_ROWS_THREADS = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(PANEL_ROWS_THREADS) qr_panel_rows_kernel(T* A, long long sA, int lda, int mp, int jb,
+                                                                           T* Vall, long long sV, int ldv, T* Tall,
+                                                                           long long sT, T* Pg, long long sP) {
+  constexpr bool CPX = Scalar<T>::is_complex;
+  constexpr int NW = PANEL_ROWS_THREADS / 32;
+  __shared__ double red[NW][QR_NB][CPX ? 2 : 1];
+  __shared__ double rs[NW];
+  __shared__ T bc[QR_NB];
+  __shared__ T s_sc, s_tau;
+  __shared__ T taus[QR_NB];
+  __shared__ T S[QR_NB][QR_NB + 1];
+  const int chain = blockIdx.x;
+  A += sA * chain;
+  Vall += sV * chain;
+  T* Tp = Tall + sT * chain;
+  T* P = Pg + sP * chain;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (long long idx = tid; idx < (long long)mp * jb; idx += PANEL_ROWS_THREADS) {
+    const int c = (int)(idx / mp), r = (int)(idx % mp);
+    P[idx] = A[(size_t)r * lda + c];
+  }
+  __syncthreads();
+  const int jr = jb < mp ? jb : mp;
+  for (int j = 0; j < jr; ++j) {
+    T* v = P + (size_t)j * mp;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < mp; i += PANEL_ROWS_THREADS) part += abs2(v[i]);
+    part = warp_sum(part);
+    if (lane == 0) rs[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double xn2 = 0.0;
+      for (int w = 0; w < NW; ++w) xn2 += rs[w];
+      const T alpha = v[j];
+      double ar, ai;
+      if constexpr (CPX) {
+        ar = alpha.x;
+        ai = alpha.y;
+      } else {
+        ar = alpha;
+        ai = 0.0;
+      }
+      T t = Scalar<T>::zero();
+      T sc = Scalar<T>::one();
+      if (!(xn2 == 0.0 && ai == 0.0)) {
+        const double beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+        if constexpr (CPX) {
+          t = cplx{(beta - ar) / beta, -ai / beta};
+          const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+          sc = cplx{dr / den, -di / den};
+          v[j] = cplx{beta, 0.0};
+        } else {
+          t = (beta - ar) / beta;
+          sc = 1.0 / (ar - beta);
+          v[j] = beta;
+        }
+      }
+      s_tau = t;
+      s_sc = sc;
+      taus[j] = t;
+    }
+    __syncthreads();
+    const T sc = s_sc;
+    for (int i = j + 1 + tid; i < mp; i += PANEL_ROWS_THREADS) v[i] = mul(v[i], sc);
+    // all trailing dots w_c = v^H P[:, c] at once (own rows; v_j = 1)
+    const int nc = jb - j - 1;
+    if (nc > 0) {
+      double pr[QR_NB], pi[QR_NB];
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) {
+        pr[c] = 0.0;
+        pi[c] = 0.0;
+      }
+      for (int i = j + tid; i < mp; i += PANEL_ROWS_THREADS) {
+        const T vi = (i == j) ? Scalar<T>::one() : v[i];
+#pragma unroll
+        for (int c = 0; c < QR_NB; ++c) {
+          if (c < nc) {
+            const T x = cmul(vi, P[(size_t)(j + 1 + c) * mp + i]);
+            if constexpr (CPX) {
+              pr[c] += x.x;
+              pi[c] += x.y;
+            } else {
+              pr[c] += x;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) {
+        if (c < nc) {
+          pr[c] = warp_sum(pr[c]);
+          if constexpr (CPX) pi[c] = warp_sum(pi[c]);
+          if (lane == 0) {
+            red[warp][c][0] = pr[c];
+            if constexpr (CPX) red[warp][c][1] = pi[c];
+          }
+        }
+      }
+      __syncthreads();
+      if (tid < nc) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < NW; ++w) {
+          a += red[w][tid][0];
+          if constexpr (CPX) b += red[w][tid][1];
+        }
+        T wc;
+        if constexpr (CPX)
+          wc = cplx{a, b};
+        else
+          wc = a;
+        bc[tid] = mul(conj_(s_tau), wc);
+      }
+      __syncthreads();
+      for (int i = j + tid; i < mp; i += PANEL_ROWS_THREADS) {
+        const T vi = (i == j) ? Scalar<T>::one() : v[i];
+        for (int c = 0; c < nc; ++c) {
+          T* a = P + (size_t)(j + 1 + c) * mp;
+          a[i] = sub(a[i], mul(vi, bc[c]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write back R / V, then S = V^H V and the WY factor (as qr_panel_kernel)
+  for (long long idx = tid; idx < (long long)mp * jb; idx += PANEL_ROWS_THREADS) {
+    const int c = (int)(idx / mp), r = (int)(idx % mp);
+    const T x = P[idx];
+    A[(size_t)r * lda + c] = x;
+    Vall[(size_t)r * ldv + c] = (c >= jr) ? Scalar<T>::zero()
+                                          : (r > c ? x : (r == c ? Scalar<T>::one() : Scalar<T>::zero()));
+  }
+  for (int pr2 = warp; pr2 < jr * jr; pr2 += NW) {
+    const int a = pr2 / jr, b = pr2 % jr;
+    if (a >= b) continue;
+    T w = Scalar<T>::zero();
+    for (int i = b + lane; i < mp; i += 32) {
+      const T va = (i == a) ? Scalar<T>::one() : (i > a ? P[(size_t)a * mp + i] : Scalar<T>::zero());
+      const T vb = (i == b) ? Scalar<T>::one() : P[(size_t)b * mp + i];
+      w = add(w, cmul(va, vb));
+    }
+    if constexpr (CPX) {
+      w.x = warp_sum(w.x);
+      w.y = warp_sum(w.y);
+    } else {
+      w = warp_sum(w);
+    }
+    if (lane == 0) S[a][b] = w;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
+    for (int i = 0; i < jr; ++i) {
+      const T ti = taus[i];
+      Tp[i * QR_NB + i] = ti;
+      for (int r = 0; r < i; ++r) {
+        T acc = Scalar<T>::zero();
+        for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
+        Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void conj_transpose_kernel(const T* src, long long s_src, int rows, int cols, T* dst, long long s_dst) {
   __shared__ T tile[32][33];
@@ -694,9 +865,14 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     const int mp = m - j0;
     const size_t pbytes = (size_t)mp * jb * sizeof(T);
     const int in_smem = pbytes <= smem_limit;
-    qr_panel_kernel<T><<<chains, PANEL_THREADS, in_smem ? pbytes : 0, s>>>(
-        A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k, Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB,
-        w.sT, static_cast<T*>(w.P), w.sP, in_smem);
+    if (in_smem)
+      qr_panel_kernel<T><<<chains, PANEL_THREADS, pbytes, s>>>(
+          A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
+          Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP, 1);
+    else
+      qr_panel_rows_kernel<T><<<chains, PANEL_ROWS_THREADS, 0, s>>>(
+          A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
+          Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP);
     ++nl;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int nt = n - j0 - jb;
