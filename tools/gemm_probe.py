@@ -16,8 +16,11 @@ SHAPES = [  # (name, opA, opB, M, N, K)
     ("square 4096", 0, 0, 4096, 4096, 4096),
     ("C2 Y", 0, 0, 128, 384, 192),
 ]
+ONLY = sys.argv[1] if len(sys.argv) > 1 else None
 for cplx in (False, True):
     for name, oa, ob, M, N, K in SHAPES:
+        if ONLY and (ONLY not in name or cplx):
+            continue
         dt = torch.complex128 if cplx else torch.float64
         A = torch.randn(M * K, dtype=dt, device="cuda")
         B = torch.randn(K * N, dtype=dt, device="cuda")
