@@ -9,6 +9,7 @@
 // in shared memory when it fits, else in an L2-resident global workspace.
 #include "qr.cuh"
 
+#include <algorithm>
 #include <cfloat>
 
 namespace ttg {
@@ -470,11 +471,14 @@ template cudaError_t householder_qr<cplx>(const QrParams&, int, cudaStream_t);
 // ---------------------------------------------------------------------------
 // blocked QR
 // ---------------------------------------------------------------------------
+#include <cooperative_groups.h>
+
 #include "gemm.cuh"
 
 namespace ttg {
 namespace {
 
+namespace cg = cooperative_groups;
 constexpr int PANEL_THREADS = 512;
 
 // Factor the mp x jb panel A[j0:, j0:j0+jb] (row stride lda) in place, write the
@@ -776,6 +780,231 @@ __global__ void __launch_bounds__(PANEL_ROWS_THREADS) qr_panel_rows_kernel(T* A,
   }
 }
 
+// Tall panels of a single chain: the rows are split over a cooperative grid,
+// each CTA keeps its row block of the panel in shared memory, and every column
+// costs two grid barriers (norm reduction, then the batched trailing dots).
+constexpr int COOP_THREADS = 256;
+constexpr int COOP_MAX_CTAS = 148;
+
+template <typename T>
+__global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int lda, int mp, int jb, T* Vall, int ldv,
+                                                                     T* Tp, double* gpart, int rows_per) {
+  constexpr bool CPX = Scalar<T>::is_complex;
+  constexpr int NW = COOP_THREADS / 32;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* P = reinterpret_cast<T*>(smem_raw);  // rows_per x jb, column-major (ld = rows_per)
+  __shared__ double wred[NW][QR_NB][CPX ? 2 : 1];
+  __shared__ double rs[NW];
+  __shared__ T wcs[QR_NB];
+  __shared__ T taus[QR_NB];
+  __shared__ T S[QR_NB][QR_NB + 1];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = b * rows_per, r1 = min(mp, r0 + rows_per), nr = max(0, r1 - r0);
+  // global scratch: [0, G) norm partials | alpha (2 doubles) | [G][QR_NB][2] dot partials | [G][QR_NB^2][2] gram
+  double* gnorm = gpart;
+  double* galpha = gpart + G;
+  double* gdot = gpart + G + 2;
+  double* ggram = gdot + (size_t)G * QR_NB * 2;
+  for (int idx = tid; idx < nr * jb; idx += COOP_THREADS) {
+    const int c = idx / nr, r = idx % nr;
+    P[c * rows_per + r] = A[(size_t)(r0 + r) * lda + c];
+  }
+  __syncthreads();
+  const int jr = jb < mp ? jb : mp;
+  for (int j = 0; j < jr; ++j) {
+    T* v = P + j * rows_per;  // local rows r0..r1-1 of column j
+    double part = 0.0;
+    for (int r = tid; r < nr; r += COOP_THREADS)
+      if (r0 + r > j) part += abs2(v[r]);
+    part = warp_sum(part);
+    if (lane == 0) rs[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t += rs[w];
+      gnorm[b] = t;
+      if (j >= r0 && j < r1) {
+        const T a = v[j - r0];
+        if constexpr (CPX) {
+          galpha[0] = a.x;
+          galpha[1] = a.y;
+        } else {
+          galpha[0] = a;
+          galpha[1] = 0.0;
+        }
+      }
+    }
+    grid.sync();
+    // every CTA forms the same reflector
+    double xn2 = 0.0;
+    for (int g = 0; g < G; ++g) xn2 += gnorm[g];
+    const double ar = galpha[0], ai = galpha[1];
+    T tau = Scalar<T>::zero(), sc = Scalar<T>::one();
+    double beta = ar;
+    const bool refl = !(xn2 == 0.0 && ai == 0.0);
+    if (refl) {
+      beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+      if constexpr (CPX) {
+        tau = cplx{(beta - ar) / beta, -ai / beta};
+        const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+        sc = cplx{dr / den, -di / den};
+      } else {
+        tau = (beta - ar) / beta;
+        sc = 1.0 / (ar - beta);
+      }
+    }
+    if (tid == 0) taus[j] = tau;
+    for (int r = tid; r < nr; r += COOP_THREADS) {
+      const int gi = r0 + r;
+      if (gi > j) v[r] = mul(v[r], sc);
+      if (gi == j && refl) {
+        if constexpr (CPX)
+          v[r] = cplx{beta, 0.0};
+        else
+          v[r] = beta;
+      }
+    }
+    __syncthreads();
+    const int nc = jb - j - 1;
+    if (nc > 0) {
+      double pr[QR_NB], pi[QR_NB];
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) {
+        pr[c] = 0.0;
+        pi[c] = 0.0;
+      }
+      for (int r = tid; r < nr; r += COOP_THREADS) {
+        const int gi = r0 + r;
+        if (gi < j) continue;
+        const T vi = (gi == j) ? Scalar<T>::one() : v[r];
+#pragma unroll
+        for (int c = 0; c < QR_NB; ++c)
+          if (c < nc) {
+            const T x = cmul(vi, P[(j + 1 + c) * rows_per + r]);
+            if constexpr (CPX) {
+              pr[c] += x.x;
+              pi[c] += x.y;
+            } else {
+              pr[c] += x;
+            }
+          }
+      }
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c)
+        if (c < nc) {
+          pr[c] = warp_sum(pr[c]);
+          if constexpr (CPX) pi[c] = warp_sum(pi[c]);
+          if (lane == 0) {
+            wred[warp][c][0] = pr[c];
+            if constexpr (CPX) wred[warp][c][1] = pi[c];
+          }
+        }
+      __syncthreads();
+      if (tid < nc) {
+        double a = 0.0, bb = 0.0;
+        for (int w = 0; w < NW; ++w) {
+          a += wred[w][tid][0];
+          if constexpr (CPX) bb += wred[w][tid][1];
+        }
+        gdot[((size_t)b * QR_NB + tid) * 2] = a;
+        gdot[((size_t)b * QR_NB + tid) * 2 + 1] = bb;
+      }
+    }
+    grid.sync();
+    if (nc > 0) {
+      if (tid < nc) {
+        double a = 0.0, bb = 0.0;
+        for (int g = 0; g < G; ++g) {
+          a += gdot[((size_t)g * QR_NB + tid) * 2];
+          bb += gdot[((size_t)g * QR_NB + tid) * 2 + 1];
+        }
+        T wc;
+        if constexpr (CPX)
+          wc = cplx{a, bb};
+        else
+          wc = a;
+        wcs[tid] = mul(conj_(tau), wc);
+      }
+      __syncthreads();
+      for (int r = tid; r < nr; r += COOP_THREADS) {
+        const int gi = r0 + r;
+        if (gi < j) continue;
+        const T vi = (gi == j) ? Scalar<T>::one() : v[r];
+        for (int c = 0; c < nc; ++c) {
+          T* a = P + (j + 1 + c) * rows_per;
+          a[r] = sub(a[r], mul(vi, wcs[c]));
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // write back R and V; Gram of V for the WY factor
+  for (int idx = tid; idx < nr * jb; idx += COOP_THREADS) {
+    const int c = idx / nr, r = idx % nr, gi = r0 + r;
+    const T x = P[c * rows_per + r];
+    A[(size_t)gi * lda + c] = x;
+    Vall[(size_t)gi * ldv + c] =
+        (c >= jr) ? Scalar<T>::zero() : (gi > c ? x : (gi == c ? Scalar<T>::one() : Scalar<T>::zero()));
+  }
+  for (int pr2 = warp; pr2 < jr * jr; pr2 += NW) {
+    const int a = pr2 / jr, c = pr2 % jr;
+    T w = Scalar<T>::zero();
+    if (a < c) {
+      for (int r = lane; r < nr; r += 32) {
+        const int gi = r0 + r;
+        const T va = (gi == a) ? Scalar<T>::one() : (gi > a ? P[a * rows_per + r] : Scalar<T>::zero());
+        const T vb = (gi == c) ? Scalar<T>::one() : (gi > c ? P[c * rows_per + r] : Scalar<T>::zero());
+        w = add(w, cmul(va, vb));
+      }
+      if constexpr (CPX) {
+        w.x = warp_sum(w.x);
+        w.y = warp_sum(w.y);
+      } else {
+        w = warp_sum(w);
+      }
+    }
+    if (lane == 0) {
+      double* gg = ggram + ((size_t)b * QR_NB * QR_NB + a * QR_NB + c) * 2;
+      if constexpr (CPX) {
+        gg[0] = w.x;
+        gg[1] = w.y;
+      } else {
+        gg[0] = w;
+        gg[1] = 0.0;
+      }
+    }
+  }
+  grid.sync();
+  if (b == 0) {
+    for (int pr2 = tid; pr2 < jr * jr; pr2 += COOP_THREADS) {
+      const int a = pr2 / jr, c = pr2 % jr;
+      double x = 0.0, y = 0.0;
+      for (int g = 0; g < G; ++g) {
+        x += ggram[((size_t)g * QR_NB * QR_NB + a * QR_NB + c) * 2];
+        y += ggram[((size_t)g * QR_NB * QR_NB + a * QR_NB + c) * 2 + 1];
+      }
+      if constexpr (CPX)
+        S[a][c] = cplx{x, y};
+      else
+        S[a][c] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
+      for (int i = 0; i < jr; ++i) {
+        const T ti = taus[i];
+        Tp[i * QR_NB + i] = ti;
+        for (int r = 0; r < i; ++r) {
+          T acc = Scalar<T>::zero();
+          for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
+          Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
+        }
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void conj_transpose_kernel(const T* src, long long s_src, int rows, int cols, T* dst, long long s_dst) {
   __shared__ T tile[32][33];
@@ -860,16 +1089,56 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   e = cudaFuncSetAttribute(qr_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
   if (e != cudaSuccess) return e;
   (void)panel_bytes_max;
+  // cooperative tall-panel path (single chain): grid scratch + occupancy
+  double* coop_part = nullptr;
+  int coop_ctas = 0;
+  if (chains == 1 && (size_t)m * QR_NB * sizeof(T) > smem_limit) {
+    const int G = COOP_MAX_CTAS;
+    const size_t rows_per = (m + G - 1) / G;
+    const size_t sm_bytes = rows_per * QR_NB * sizeof(T);
+    if (sm_bytes <= 200 * 1024) {
+      e = cudaFuncSetAttribute(qr_panel_coop_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes);
+      int per_sm = 0;
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop_kernel<T>, COOP_THREADS, sm_bytes);
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess && per_sm > 0) {
+        coop_ctas = std::min(G, sms * per_sm);
+        const size_t words = (size_t)G + 2 + (size_t)G * QR_NB * 2 + (size_t)G * QR_NB * QR_NB * 2;
+        e = cudaMallocAsync(&coop_part, words * sizeof(double), s);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          coop_part = nullptr;
+        }
+      }
+      cudaGetLastError();
+    }
+  }
   for (int j0 = 0; j0 < k; j0 += QR_NB) {
     const int jb = (k - j0) < QR_NB ? (k - j0) : QR_NB;
     const int mp = m - j0;
     const size_t pbytes = (size_t)mp * jb * sizeof(T);
     const int in_smem = pbytes <= smem_limit;
-    if (in_smem)
+    if (in_smem) {
       qr_panel_kernel<T><<<chains, PANEL_THREADS, pbytes, s>>>(
           A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
           Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP, 1);
-    else
+    } else if (chains == 1 && coop_part) {
+      const int G = std::min(COOP_MAX_CTAS, std::max(1, coop_ctas));
+      int rows_per = (mp + G - 1) / G;
+      const int Gu = (mp + rows_per - 1) / rows_per;
+      T* Ap = A + (size_t)j0 * n + j0;
+      T* Vp = V + (size_t)j0 * k + j0;
+      T* Tp = Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB;
+      int lda_ = n, mp_ = mp, jb_ = jb, ldv_ = k;
+      double* gp = coop_part;
+      void* args[] = {&Ap, &lda_, &mp_, &jb_, &Vp, &ldv_, &Tp, &gp, &rows_per};
+      e = cudaLaunchCooperativeKernel((void*)qr_panel_coop_kernel<T>, dim3(Gu), dim3(COOP_THREADS), args,
+                                      (size_t)rows_per * QR_NB * sizeof(T), s);
+      if (e != cudaSuccess) return e;
+    } else
       qr_panel_rows_kernel<T><<<chains, PANEL_ROWS_THREADS, 0, s>>>(
           A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
           Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP);
@@ -901,6 +1170,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       nl += 3;
     }
   }
+  if (coop_part) cudaFreeAsync(coop_part, s);
   upper_kernel<T><<<dim3(blocks_for((long long)k * n), chains), 256, 0, s>>>(A, w.sA, n, static_cast<T*>(p.R), p.sR, k);
   T* Q = static_cast<T*>(p.Q);
   if (!Q) {  // R only
