@@ -1089,32 +1089,27 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   e = cudaFuncSetAttribute(qr_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
   if (e != cudaSuccess) return e;
   (void)panel_bytes_max;
-  // cooperative tall-panel path (single chain): grid scratch + occupancy
+  // cooperative tall-panel path (single chain): one CTA per SM at most, <= 200 KB
+  // of panel rows per CTA (occupancy checked for the largest launch below)
   double* coop_part = nullptr;
   int coop_ctas = 0;
+  const size_t coop_smem_max = 200 * 1024;
   if (chains == 1 && (size_t)m * QR_NB * sizeof(T) > smem_limit) {
-    const int G = COOP_MAX_CTAS;
-    const size_t rows_per = (m + G - 1) / G;
-    const size_t sm_bytes = rows_per * QR_NB * sizeof(T);
-    if (sm_bytes <= 200 * 1024) {
-      e = cudaFuncSetAttribute(qr_panel_coop_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes);
-      int per_sm = 0;
-      if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop_kernel<T>, COOP_THREADS, sm_bytes);
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (e == cudaSuccess && per_sm > 0) {
-        coop_ctas = std::min(G, sms * per_sm);
-        const size_t words = (size_t)G + 2 + (size_t)G * QR_NB * 2 + (size_t)G * QR_NB * QR_NB * 2;
-        e = cudaMallocAsync(&coop_part, words * sizeof(double), s);
-        if (e != cudaSuccess) {
-          cudaGetLastError();
-          coop_part = nullptr;
-        }
-      }
-      cudaGetLastError();
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaFuncSetAttribute(qr_panel_coop_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_max);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop_kernel<T>, COOP_THREADS, coop_smem_max);
+    if (e == cudaSuccess && per_sm > 0) {
+      coop_ctas = std::min(COOP_MAX_CTAS, sms);
+      const size_t words = (size_t)COOP_MAX_CTAS + 2 + (size_t)COOP_MAX_CTAS * QR_NB * 2 +
+                           (size_t)COOP_MAX_CTAS * QR_NB * QR_NB * 2;
+      e = cudaMallocAsync(&coop_part, words * sizeof(double), s);
+      if (e != cudaSuccess) coop_part = nullptr;
     }
+    cudaGetLastError();
+    e = cudaSuccess;
   }
   for (int j0 = 0; j0 < k; j0 += QR_NB) {
     const int jb = (k - j0) < QR_NB ? (k - j0) : QR_NB;
@@ -1125,8 +1120,10 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       qr_panel_kernel<T><<<chains, PANEL_THREADS, pbytes, s>>>(
           A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
           Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP, 1);
-    } else if (chains == 1 && coop_part) {
-      const int G = std::min(COOP_MAX_CTAS, std::max(1, coop_ctas));
+    } else if (chains == 1 && coop_part &&
+               (size_t)((mp + coop_ctas - 1) / coop_ctas) * QR_NB * sizeof(T) <= coop_smem_max) {
+      // at least 128 rows per CTA: fewer CTAs make the two grid barriers per column cheaper
+      const int G = std::max(1, std::min(coop_ctas, (mp + 127) / 128));
       int rows_per = (mp + G - 1) / G;
       const int Gu = (mp + rows_per - 1) / rows_per;
       T* Ap = A + (size_t)j0 * n + j0;
