@@ -252,7 +252,7 @@ struct Engine {
                    K.eval(hb.data(), c, ld);
     GemmParams p{A, Bm, C, sA, sB, sC, M, N, K, d_bonds, ld, check_active ? d_state : nullptr, 1.0, beta};
     ProfScope ps(ctx, TTG_PROF_GEMM, flops);
-    CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st));
+    CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st, ub(K)));
     ++ctx->launches;
   }
 

@@ -5,6 +5,8 @@
 // (complex) fragment loads are bank-conflict free.
 #include "gemm.cuh"
 
+#include <algorithm>
+
 namespace ttg {
 namespace {
 
@@ -123,12 +125,18 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
     }
   };
 
-  const int ktiles = (K + BK - 1) / BK;
-  if (ktiles > 0) load_tile(0, 0);
+  // split-K: blockIdx.z owns k-tiles [kt0, kt1); partial tiles are added atomically
+  const int ktiles_all = (K + BK - 1) / BK;
+  const int splits = gridDim.z;
+  const int per = (ktiles_all + splits - 1) / splits;
+  const int kt0 = blockIdx.z * per;
+  const int kt1 = min(ktiles_all, kt0 + per);
+  const int ktiles = max(0, kt1 - kt0);
+  if (ktiles > 0) load_tile(0, kt0 * BK);
   cp_commit();
   for (int kt = 0; kt < ktiles; ++kt) {
     const int stage = kt & 1;
-    if (kt + 1 < ktiles) load_tile(stage ^ 1, (kt + 1) * BK);
+    if (kt + 1 < ktiles) load_tile(stage ^ 1, (kt0 + kt + 1) * BK);
     cp_commit();
     cp_wait<1>();
     __syncthreads();
@@ -189,7 +197,14 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int n = n0 + wn + j * 8 + 2 * t4 + (r & 1);
         if (m < M && n < N) {
           T* dst = C + m * ldc + n;
-          if constexpr (!CPX) {
+          if (splits > 1) {  // C was zeroed (beta == 0) or holds the accumuland (beta == 1)
+            if constexpr (!CPX) {
+              atomicAdd(dst, alpha * acc[i][j][r]);
+            } else {
+              atomicAdd(&dst->x, alpha * acc[i][j][r]);
+              atomicAdd(&dst->y, alpha * acci[i][j][r]);
+            }
+          } else if constexpr (!CPX) {
             const double v = alpha * acc[i][j][r];
             *dst = p.beta ? *dst + v : v;
           } else {
@@ -199,6 +214,21 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
           }
         }
       }
+}
+
+template <typename T>
+__global__ void zero_c_kernel(GemmParams p) {
+  const int chain = blockIdx.y;
+  if (p.st && !p.st[chain].active) return;
+  const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
+  const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
+  const long long ldc = p.ldc ? p.ldc : N;
+  T* C = static_cast<T*>(p.C) + p.sC * chain;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)M * N;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / N, n = idx % N;
+    C[m * ldc + n] = Scalar<T>::zero();
+  }
 }
 
 template <typename T, int OPA>
@@ -215,10 +245,22 @@ cudaError_t launch_b(const GemmParams& p, int opB, dim3 grid, int tiles_n, cudaS
 }  // namespace
 
 template <typename T>
-cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int chains, cudaStream_t s) {
+cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int chains, cudaStream_t s, int kmax) {
   if (mmax <= 0 || nmax <= 0 || chains <= 0) return cudaSuccess;
   const int tiles_m = (mmax + BM - 1) / BM, tiles_n = (nmax + BN - 1) / BN;
-  dim3 grid(tiles_m * tiles_n, chains);
+  // split-K when the output tiles cannot fill the GPU but K is long (e.g. V^H A in the
+  // blocked QR: 32 x n x m)
+  int splits = 1;
+  const long long tiles = (long long)tiles_m * tiles_n * chains;
+  if (kmax >= 1024 && tiles < 2 * 148) {
+    splits = (int)std::min<long long>((2 * 148 + tiles - 1) / tiles, kmax / 256);
+    splits = std::max(1, std::min(splits, 64));
+  }
+  if (splits > 1 && p.beta == 0) {
+    zero_c_kernel<T><<<dim3(std::max(1, std::min(148 * 4, (int)((long long)mmax * nmax / 256 + 1))), chains), 256, 0,
+                       s>>>(p);
+  }
+  dim3 grid(tiles_m * tiles_n, chains, splits);
   switch (opA) {
     case OP_N: return launch_b<T, OP_N>(p, opB, grid, tiles_n, s);
     case OP_T: return launch_b<T, OP_T>(p, opB, grid, tiles_n, s);
@@ -227,7 +269,7 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
   }
 }
 
-template cudaError_t gemm<double>(const GemmParams&, int, int, int, int, int, cudaStream_t);
-template cudaError_t gemm<cplx>(const GemmParams&, int, int, int, int, int, cudaStream_t);
+template cudaError_t gemm<double>(const GemmParams&, int, int, int, int, int, cudaStream_t, int);
+template cudaError_t gemm<cplx>(const GemmParams&, int, int, int, int, int, cudaStream_t, int);
 
 }  // namespace ttg

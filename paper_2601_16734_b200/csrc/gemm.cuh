@@ -28,8 +28,9 @@ struct GemmParams {
   long long lda = 0, ldb = 0, ldc = 0;
 };
 
-// Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only).
+// Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only);
+// kmax (an upper bound of K, 0 = unknown) enables split-K for long, narrow products.
 template <typename T>
-cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int chains, cudaStream_t s);
+cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int chains, cudaStream_t s, int kmax = 0);
 
 }  // namespace ttg

@@ -1149,7 +1149,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       g1.lda = k;
       g1.ldb = n;
       g1.ldc = nt;
-      if ((e = gemm<T>(g1, OP_C, OP_N, jb, nt, chains, s)) != cudaSuccess) return e;
+      if ((e = gemm<T>(g1, OP_C, OP_N, jb, nt, chains, s, mp)) != cudaSuccess) return e;
       // W2 = T^H W1
       GemmParams g2{Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(nt),
                     dconst(jb), nullptr, 0, nullptr, 1.0, 0};
@@ -1187,7 +1187,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     g1.lda = k;
     g1.ldb = k;
     g1.ldc = kq;
-    if ((e = gemm<T>(g1, OP_C, OP_N, jb, kq, chains, s)) != cudaSuccess) return e;
+    if ((e = gemm<T>(g1, OP_C, OP_N, jb, kq, chains, s, mp)) != cudaSuccess) return e;
     // W2 = T W1
     GemmParams g2{Tt + (size_t)b * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(kq), dconst(jb),
                   nullptr, 0, nullptr, 1.0, 0};
