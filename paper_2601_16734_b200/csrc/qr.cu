@@ -786,12 +786,23 @@ __global__ void __launch_bounds__(PANEL_ROWS_THREADS) qr_panel_rows_kernel(T* A,
 constexpr int COOP_THREADS = 256;
 constexpr int COOP_MAX_CTAS = 148;
 
-template <typename T>
+template <bool CLUSTER>
+__device__ __forceinline__ void panel_barrier() {
+  if constexpr (CLUSTER) {
+    __threadfence();
+    cg::this_cluster().sync();
+  } else {
+    cg::this_grid().sync();
+  }
+}
+
+// CLUSTER: the CTAs form one thread-block cluster (<= 16) and synchronise with
+// the hardware cluster barrier; otherwise a cooperative grid barrier.
+template <typename T, bool CLUSTER>
 __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int lda, int mp, int jb, T* Vall, int ldv,
                                                                      T* Tp, double* gpart, int rows_per) {
   constexpr bool CPX = Scalar<T>::is_complex;
   constexpr int NW = COOP_THREADS / 32;
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* P = reinterpret_cast<T*>(smem_raw);  // rows_per x jb, column-major (ld = rows_per)
   __shared__ double wred[NW][QR_NB][CPX ? 2 : 1];
@@ -835,7 +846,7 @@ __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int l
         }
       }
     }
-    grid.sync();
+    panel_barrier<CLUSTER>();
     // every CTA forms the same reflector
     double xn2 = 0.0;
     for (int g = 0; g < G; ++g) xn2 += gnorm[g];
@@ -911,7 +922,7 @@ __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int l
         gdot[((size_t)b * QR_NB + tid) * 2 + 1] = bb;
       }
     }
-    grid.sync();
+    panel_barrier<CLUSTER>();
     if (nc > 0) {
       if (tid < nc) {
         double a = 0.0, bb = 0.0;
@@ -975,7 +986,7 @@ __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int l
       }
     }
   }
-  grid.sync();
+  panel_barrier<CLUSTER>();
   if (b == 0) {
     for (int pr2 = tid; pr2 < jr * jr; pr2 += COOP_THREADS) {
       const int a = pr2 / jr, c = pr2 % jr;
@@ -1098,9 +1109,16 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaFuncSetAttribute(qr_panel_coop_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_max);
+    e = cudaFuncSetAttribute(qr_panel_coop_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)coop_smem_max);
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop_kernel<T>, COOP_THREADS, coop_smem_max);
+      e = cudaFuncSetAttribute(qr_panel_coop_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)coop_smem_max);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(qr_panel_coop_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop_kernel<T, false>, COOP_THREADS,
+                                                        coop_smem_max);
     if (e == cudaSuccess && per_sm > 0) {
       coop_ctas = std::min(COOP_MAX_CTAS, sms);
       const size_t words = (size_t)COOP_MAX_CTAS + 2 + (size_t)COOP_MAX_CTAS * QR_NB * 2 +
@@ -1131,10 +1149,33 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       T* Tp = Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB;
       int lda_ = n, mp_ = mp, jb_ = jb, ldv_ = k;
       double* gp = coop_part;
-      void* args[] = {&Ap, &lda_, &mp_, &jb_, &Vp, &ldv_, &Tp, &gp, &rows_per};
-      e = cudaLaunchCooperativeKernel((void*)qr_panel_coop_kernel<T>, dim3(Gu), dim3(COOP_THREADS), args,
-                                      (size_t)rows_per * QR_NB * sizeof(T), s);
-      if (e != cudaSuccess) return e;
+      const size_t pbytes2 = (size_t)rows_per * QR_NB * sizeof(T);
+      bool launched = false;
+      if (Gu <= 16) {  // one thread-block cluster: hardware cluster barrier
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(Gu);
+        cfg.blockDim = dim3(COOP_THREADS);
+        cfg.dynamicSmemBytes = pbytes2;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = Gu;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, qr_panel_coop_kernel<T, true>, Ap, lda_, mp_, jb_, Vp, ldv_, Tp, gp, rows_per);
+        if (e == cudaSuccess)
+          launched = true;
+        else
+          cudaGetLastError();
+      }
+      if (!launched) {
+        void* args[] = {&Ap, &lda_, &mp_, &jb_, &Vp, &ldv_, &Tp, &gp, &rows_per};
+        e = cudaLaunchCooperativeKernel((void*)qr_panel_coop_kernel<T, false>, dim3(Gu), dim3(COOP_THREADS), args,
+                                        pbytes2, s);
+        if (e != cudaSuccess) return e;
+      }
     } else
       qr_panel_rows_kernel<T><<<chains, PANEL_ROWS_THREADS, 0, s>>>(
           A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
