@@ -24,7 +24,13 @@ def run(th, mode, tol_rot):
 rng = np.random.default_rng(0)
 if len(sys.argv) > 1:
     m = n = int(sys.argv[1])
-    print(run(rng.standard_normal((m, n)), 0, 0.0))
+    A = rng.standard_normal((m, n))
+    if len(sys.argv) > 2:  # graded spectrum exp(-k/decay)
+        U, _ = np.linalg.qr(rng.standard_normal((m, m)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        A = (U * np.exp(-np.arange(m) / float(sys.argv[2]))) @ V.T
+    run(A, 0, 0.0)  # warm-up (module load, smem attribute)
+    print(run(A, 0, 0.0), run(A, 1, 0.0))
     sys.exit(0)
 for (m, n) in [(32, 32), (64, 64), (128, 128), (192, 128), (128, 192), (256, 256)]:
     for decay in (False, True):
