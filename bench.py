@@ -113,27 +113,83 @@ def workload(cfg_name, rank, world=1, chains=None):
         total = chains or cfg.batch
         lo, hi = shard_range(total, world, rank)
         return cfg, [I.config_inputs(cfg, chain=c)[0][0] for c in range(lo, hi)], None
-    if cfg.kind != "apply":
-        raise SystemExit(f"bench workload must be an apply or batch config, got {cfg_name}")
     import dataclasses
     cfg_r = dataclasses.replace(cfg, seed=cfg.seed + 1000 * rank)
-    (psi,), W = I.config_inputs(cfg_r)
-    return cfg, psi, W
+    mps, W = I.config_inputs(cfg_r)
+    return cfg, mps, W
 
 
-def cpu_reference(cfg, psi, W, steps, warmup, threads):
+def _call(ttlab, cfg, mps, W, strat, rep=None):
+    """One call of the config's hot path (device objects or host tensors)."""
+    if cfg.kind == "apply":
+        return ttlab.apply(W, mps[0], strat, report=rep)
+    if cfg.kind == "hadamard":
+        return ttlab.simplify(ttlab.hadamard(mps[0], mps[1]), strat, report=rep)
+    return ttlab.simplify(mps[0], strat, report=rep)
+
+
+def _target_bonds(cfg, mps, W):
+    if cfg.kind == "apply":
+        return [1] + [w.shape[3] * a.shape[2] for w, a in zip(W, mps[0])]
+    if cfg.kind == "hadamard":
+        return [1] + [a.shape[2] * b.shape[2] for a, b in zip(mps[0], mps[1])]
+    return [1] + [a.shape[2] for a in mps[0]]
+
+
+def cpu_step_estimate(cfg, mps, W, threads):
+    """Bounded CPU sample for the large configs (C3/C4): one middle two-site
+    step of the sweep in reference arithmetic (pair-first project_pair,
+    forms.hpp:13-32, then schmidt_split) on the real target tensors, timed and
+    extrapolated to 2(n-1) steps per sweep (the QR pass is not included)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    import numpy as np
+    from oracle import ttlab_oracle as O
+    n = cfg.n // 2 - 1
+    if cfg.kind == "apply":
+        sites = []
+        for k in (n, n + 1):
+            w, a = W[k].astype(np.complex128), mps[0][k].astype(np.complex128)
+            c = np.einsum("cjid,aib->cajdb", w, a)
+            sites.append(c.reshape(w.shape[0] * a.shape[0], w.shape[1], w.shape[3] * a.shape[2]))
+    else:
+        sites = []
+        for k in (n, n + 1):
+            a, b = mps[0][k], mps[1][k]
+            c = np.einsum("asc,bsd->abscd", a, b)
+            sites.append(c.reshape(a.shape[0] * b.shape[0], a.shape[1], a.shape[2] * b.shape[2]))
+    p = cfg.out_chi
+    rng = np.random.default_rng(0)
+    L = rng.standard_normal((p, sites[0].shape[0])) + 1j * rng.standard_normal((p, sites[0].shape[0]))
+    R = rng.standard_normal((p, sites[1].shape[2])) + 1j * rng.standard_normal((p, sites[1].shape[2]))
+    t0 = time.perf_counter()
+    f = O.project_pair(L, sites[0], sites[1], R)
+    O.split_pair(f, 2, 2, O.Strategy(max_bond=p, tolerance=cfg.tolerance), O.LEFT_TO_RIGHT)
+    step = time.perf_counter() - t0
+    per_sweep = 2 * (cfg.n - 1) * step
+    return 1.0 / per_sweep, step
+
+
+def cpu_reference(cfg, mps, W, steps, warmup, threads):
     """Time the oracle restatement (reference arithmetic: complex128 promotion,
     pair-first project_pair, scprod <T,T>) on the host cores."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     from oracle import ttlab_oracle as O
     strat = O.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
-    mpo, mps = O.MPO(W), O.MPS(psi)
+    ms = [O.MPS(m) for m in mps]
+
+    def once(rep=None):
+        if cfg.kind == "apply":
+            return O.apply(O.MPO(W), ms[0], strat, promote=True, report=rep)
+        if cfg.kind == "hadamard":
+            return O.simplify(O.hadamard(ms[0], ms[1]), strat, promote=True, report=rep)
+        return O.simplify(ms[0], strat, promote=True, report=rep)
+
     for _ in range(warmup):
-        O.apply(mpo, mps, strat, promote=True)
+        once()
     sweeps, t0 = 0, time.perf_counter()
     for _ in range(steps):
         rep = {}
-        O.apply(mpo, mps, strat, promote=True, report=rep)
+        once(rep)
         sweeps += rep["sweeps"]
     dt = time.perf_counter() - t0
     return sweeps / dt, dt, sweeps
@@ -163,8 +219,8 @@ def run_reference(args):
                 "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
-    cfg, psi, W = workload(args.config, 0)
-    val, dt, sweeps = cpu_reference(cfg, psi, W, args.steps, min(args.warmup, 1), threads)
+    cfg, mps, W = workload(args.config, 0)
+    val, dt, sweeps = cpu_reference(cfg, mps, W, args.steps, min(args.warmup, 1), threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "sweeps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * dt / args.steps,
@@ -179,9 +235,15 @@ def run_reference(args):
 
 
 def _workload_desc(cfg):
-    mpo = "QTT Laplacian D=3" if cfg.mpo_D == 3 else f"random MPO D={cfg.mpo_D}"
-    return (f"{cfg.name}: {mpo} applied to n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS (seed {cfg.seed}+1000*rank), "
-            f"simplify to chi={cfg.out_chi}, tol {cfg.tolerance:g}, max {cfg.max_sweeps} sweeps")
+    tail = f"simplify to chi={cfg.out_chi}, tol {cfg.tolerance:g}, max {cfg.max_sweeps} sweeps"
+    if cfg.kind == "apply":
+        mpo = "QTT Laplacian D=3" if cfg.mpo_D == 3 else f"random MPO D={cfg.mpo_D}"
+        return (f"{cfg.name}: {mpo} applied to n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS (seed {cfg.seed}+1000*rank), "
+                + tail)
+    if cfg.kind == "hadamard":
+        return (f"{cfg.name}: Hadamard product of two n={cfg.n} d={cfg.d} chi={cfg.chi} complex128 MPS "
+                f"(seeds {cfg.seed}/{cfg.seed + 1}), " + tail)
+    return f"{cfg.name}: n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS (seed {cfg.seed}+1000*rank), " + tail
 
 
 def run_ours(args):
@@ -197,15 +259,15 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    cfg, psi, W = workload(args.config, rank)
+    cfg, mps, W = workload(args.config, rank)
     strat = ttlab.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
 
     ctx = ttlab.context(local)
     stream = torch.cuda.Stream(dev)  # a real stream: the library and the events share it
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    Wd = ttlab.DeviceMPO(W, ctx=ctx)
-    psid = ttlab.DeviceMPS.from_tensors(psi, ctx=ctx)
+    Wd = ttlab.DeviceMPO(W, ctx=ctx) if W is not None else None
+    mpsd = [ttlab.DeviceMPS.from_tensors(m, ctx=ctx) for m in mps]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -214,7 +276,7 @@ def run_ours(args):
 
     # warm-up
     for _ in range(args.warmup):
-        out = ttlab.apply(Wd, psid, strat)
+        out = _call(ttlab, cfg, mpsd, Wd, strat)
     torch.cuda.synchronize()
 
     # ---- timed: device-resident inputs
@@ -230,7 +292,7 @@ def run_ours(args):
         flush.zero_()  # L2 flush between timed steps (outside the events)
         rep = []
         ev[i][0].record(stream)
-        out = ttlab.apply(Wd, psid, strat, report=rep)
+        out = _call(ttlab, cfg, mpsd, Wd, strat, rep)
         ev[i][1].record(stream)
         sweeps += rep[0]["sweeps"]
         reps.append(rep[0])
@@ -243,18 +305,18 @@ def run_ours(args):
 
     # ---- e2e through the public host API (H2D + call + D2H every step)
     for _ in range(1):
-        ttlab.apply(W, psi, strat).to_tensors()
+        _call(ttlab, cfg, mps, W, strat).to_tensors()
     torch.cuda.synchronize()
     barrier()
     e2e_sweeps, t_e2e = 0, 0.0
-    h2d = sum(a.nbytes for a in psi) + sum(np.asarray(w).nbytes for w in W)
+    h2d = sum(a.nbytes for m in mps for a in m) + (sum(np.asarray(w).nbytes for w in W) if W is not None else 0)
     d2h = 0
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rep = []
-        res = ttlab.apply(W, psi, strat, report=rep).to_tensors()
+        res = _call(ttlab, cfg, mps, W, strat, rep).to_tensors()
         t_e2e += time.perf_counter() - t0
         e2e_sweeps += rep[0]["sweeps"]
         d2h = sum(a.nbytes for a in res)
@@ -277,15 +339,15 @@ def run_ours(args):
     e2e_value = total_e2e_sweeps / (e2e_ms_max / 1e3)
 
     # ---- algorithmic work and roofline (profiled pass, separate from the timed one)
-    t_b = [1] + [w.shape[3] * a.shape[2] for w, a in zip(W, psi)]
-    fl = F.algorithmic_flops(t_b, out_bonds, [2] * cfg.n, int(round(sweeps / args.steps)))
+    t_b = _target_bonds(cfg, mps, W)
+    fl = F.algorithmic_flops(t_b, out_bonds, [2] * cfg.n, int(round(sweeps / args.steps)), complex_=cfg.complex_)
     f_alg = fl["F_alg"]
     tflops = f_alg / (ms / args.steps / 1e3) / 1e12
     roofline = None
     prof = None
     if not args.no_profile:
         ctx.profile_enable(True)
-        ttlab.apply(Wd, psid, strat)
+        _call(ttlab, cfg, mpsd, Wd, strat)
         prof = ctx.profile_read()
         ctx.profile_enable(False)
         dom = max(("gemm", "svd", "qr"), key=lambda k: prof[k]["ms"])
@@ -309,16 +371,23 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, dt, sw = cpu_reference(cfg, psi, W, 1, 0, threads)
-        cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port",
-               "sample": f"1 full {cfg.name} apply+simplify call ({sw} sweeps, {dt:.1f} s), numpy/scipy restatement "
-                         "(oracle/) in reference arithmetic (complex128 promotion, pair-first projection)"}
+        if cfg.name in ("C3", "C4"):
+            v, step = cpu_step_estimate(cfg, mps, W, threads)
+            cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port",
+                   "sample": f"one middle two-site step of {cfg.name} ({step:.1f} s: pair-first project_pair + "
+                             f"schmidt_split, complex128) extrapolated to {2 * (cfg.n - 1)} steps per sweep; "
+                             "QR pass excluded (partial)"}
+        else:
+            v, dt, sw = cpu_reference(cfg, mps, W, 1, 0, threads)
+            cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port",
+                   "sample": f"1 full {cfg.name} call ({sw} sweeps, {dt:.1f} s), numpy/scipy restatement "
+                             "(oracle/) in reference arithmetic (complex128 promotion, pair-first projection)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128" if cfg.complex_ else "f64", "data": "synthetic",
             "config": {"workload": _workload_desc(cfg), "global_batch": world, "chains_per_gpu": 1,
                        "parallelism": f"dp{world} (independent chains)", "l2": "flushed between steps (512 MiB write)",
                        "output_bonds_max": max(out_bonds)},

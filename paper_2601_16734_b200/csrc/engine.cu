@@ -379,8 +379,16 @@ void Engine<T>::split_preconditioned(const void* theta, long long s_theta, DimEx
   const DimExpr R0 = dbond(pre_slot);
   const int lu = ub(Lr), ku = ub(Kc);
   const ChainState* stp = check_active ? d_state : nullptr;
+  double qflops = 0.0;  // QR with Q: 4n^2(m - n/3); R only: 2n^2(m - n/3)
+  if (live_dims(check_active))
+    for (int c = 0; c < B; ++c)
+      if (chain_on(c, check_active)) {
+        const double a = std::max(Lr.eval(hb.data(), c, ld), Kc.eval(hb.data(), c, ld));
+        const double b = std::min(Lr.eval(hb.data(), c, ld), Kc.eval(hb.data(), c, ld));
+        qflops += (Scalar<T>::is_complex ? 4.0 : 1.0) * 6.0 * b * b * (a - b / 3.0);
+      }
   {
-    ProfScope ps(ctx, TTG_PROF_QR, 0.0);
+    ProfScope ps(ctx, TTG_PROF_QR, qflops);
     CK(qr_precondition<T>(theta, s_theta, M, N, mode, d_bonds, ld, pre_slot, Qb, sp, R1h, sp, lu, ku, stp, B, st));
     CK(qr_precondition<T>(R1h, sp, Kc, R0, 0, d_bonds, ld, pre_slot, nullptr, 0, Lb, sp, ku, std::min(lu, ku), stp, B,
                           st));
