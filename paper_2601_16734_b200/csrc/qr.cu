@@ -481,6 +481,25 @@ namespace {
 namespace cg = cooperative_groups;
 constexpr int PANEL_THREADS = 512;
 
+// xLARFT (forward, columnwise) by one warp: T[i,i] = tau_i,
+// T[0:i,i] = -tau_i T[0:i,0:i] S[0:i,i]; lane r owns row r of T and only reads
+// back its own row (global Tp, no shared-memory copy).
+template <typename T>
+__device__ __forceinline__ void warp_larft(const T (&S)[QR_NB][QR_NB + 1], const T* taus, int jr, int lane, T* Tp) {
+  T* row = Tp + lane * QR_NB;
+  for (int c = 0; c < QR_NB; ++c) row[c] = Scalar<T>::zero();
+  for (int i = 0; i < jr; ++i) {
+    const T ti = taus[i];
+    if (lane < i) {
+      T acc = Scalar<T>::zero();
+      for (int c = lane; c < i; ++c) acc = add(acc, mul(row[c], S[c][i]));
+      row[i] = mul(sub(Scalar<T>::zero(), ti), acc);
+    } else if (lane == i) {
+      row[i] = ti;
+    }
+  }
+}
+
 // Factor the mp x jb panel A[j0:, j0:j0+jb] (row stride lda) in place, write the
 // unit lower-trapezoidal V into Vall[j0:, j0:j0+jb] (row stride k) and the
 // jb x jb upper-triangular WY factor into Tp.
@@ -595,18 +614,7 @@ __global__ void __launch_bounds__(PANEL_THREADS) qr_panel_kernel(T* A, long long
   }
   __syncthreads();
   // xLARFT (forward, columnwise): T[i,i] = tau_i, T[0:i,i] = -tau_i T[0:i,0:i] S[0:i,i]
-  if (tid == 0) {
-    for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
-    for (int i = 0; i < jr; ++i) {
-      const T ti = taus[i];
-      Tp[i * QR_NB + i] = ti;
-      for (int r = 0; r < i; ++r) {
-        T acc = Scalar<T>::zero();
-        for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
-        Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
-      }
-    }
-  }
+  if (warp == 0) warp_larft<T>(S, taus, jr, lane, Tp);
 }
 
 // Tall panels (not in shared memory): rows are spread over 1024 threads, the
@@ -766,18 +774,7 @@ __global__ void __launch_bounds__(PANEL_ROWS_THREADS) qr_panel_rows_kernel(T* A,
     if (lane == 0) S[a][b] = w;
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
-    for (int i = 0; i < jr; ++i) {
-      const T ti = taus[i];
-      Tp[i * QR_NB + i] = ti;
-      for (int r = 0; r < i; ++r) {
-        T acc = Scalar<T>::zero();
-        for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
-        Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
-      }
-    }
-  }
+  if (warp == 0) warp_larft<T>(S, taus, jr, lane, Tp);
 }
 
 // Tall panels of a single chain: the rows are split over a cooperative grid,
@@ -1001,18 +998,7 @@ __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int l
         S[a][c] = x;
     }
     __syncthreads();
-    if (tid == 0) {
-      for (int i = 0; i < QR_NB * QR_NB; ++i) Tp[i] = Scalar<T>::zero();
-      for (int i = 0; i < jr; ++i) {
-        const T ti = taus[i];
-        Tp[i * QR_NB + i] = ti;
-        for (int r = 0; r < i; ++r) {
-          T acc = Scalar<T>::zero();
-          for (int c = r; c < i; ++c) acc = add(acc, mul(Tp[r * QR_NB + c], S[c][i]));
-          Tp[r * QR_NB + i] = mul(sub(Scalar<T>::zero(), ti), acc);
-        }
-      }
-    }
+    if (warp == 0) warp_larft<T>(S, taus, jr, lane, Tp);
   }
 }
 
