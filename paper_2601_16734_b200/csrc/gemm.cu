@@ -42,8 +42,18 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
   constexpr int KSH = BK == 16 ? 4 : 3;
   constexpr int SA = BM + PAD, SB = BN + PAD;
   constexpr bool CPX = Scalar<T>::is_complex;
-  __shared__ __align__(16) T As[STAGES][BK][SA];
-  __shared__ __align__(16) T Bs[STAGES][BK][SB];
+  // Operands whose global layout is contiguous along k are staged [row][k]
+  // (stride BK + 4: conflict-free fragment loads and conflict-free cp.async
+  // stores); the others [k][row] (stride BM + PAD).
+  constexpr bool AK = (OPA == OP_N || OPA == OP_R);
+  constexpr bool BK_ = (OPB == OP_T || OPB == OP_C);
+  constexpr int SK = BK + 4;
+  constexpr int A_ELEMS = AK ? BM * SK : BK * SA;
+  constexpr int B_ELEMS = BK_ ? BN * SK : BK * SB;
+  __shared__ __align__(16) T As[STAGES][A_ELEMS];
+  __shared__ __align__(16) T Bs[STAGES][B_ELEMS];
+  auto a_at = [&](int st, int k, int m) -> T& { return AK ? As[st][m * SK + k] : As[st][k * SA + m]; };
+  auto b_at = [&](int st, int k, int n) -> T& { return BK_ ? Bs[st][n * SK + k] : Bs[st][k * SB + n]; };
 
   const int chain = blockIdx.y;
   if (p.st && !p.st[chain].active) return;
@@ -91,7 +101,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int m = mb + (NTHREADS / BK) * i;
         const bool v = (m0 + m < M) && (k0 + kk < K);
         const T* src = v ? A + (m0 + m) * lda + (k0 + kk) : A;
-        cp_async(&As[stage][kk][m], src, v, sizeof(T));
+        cp_async(&a_at(stage, kk, m), src, v, sizeof(T));
       }
     } else {
       const int m = tid & 63, kb = tid >> 6;
@@ -100,7 +110,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int kk = kb + 2 * i;
         const bool v = (m0 + m < M) && (k0 + kk < K);
         const T* src = v ? A + (k0 + kk) * lda + (m0 + m) : A;
-        cp_async(&As[stage][kk][m], src, v, sizeof(T));
+        cp_async(&a_at(stage, kk, m), src, v, sizeof(T));
       }
     }
     // B tile: BK x BN, element (k, n) -> Bs[k][n]
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int kk = kb + 2 * i;
         const bool v = (n0 + n < N) && (k0 + kk < K);
         const T* src = v ? B + (k0 + kk) * ldb + (n0 + n) : B;
-        cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
+        cp_async(&b_at(stage, kk, n), src, v, sizeof(T));
       }
     } else {
       const int kk = tid & (BK - 1), nb = tid >> KSH;
@@ -120,7 +130,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int n = nb + (NTHREADS / BK) * i;
         const bool v = (n0 + n < N) && (k0 + kk < K);
         const T* src = v ? B + (n0 + n) * ldb + (k0 + kk) : B;
-        cp_async(&Bs[stage][kk][n], src, v, sizeof(T));
+        cp_async(&b_at(stage, kk, n), src, v, sizeof(T));
       }
     }
   };
@@ -146,11 +156,11 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         double a[2][2], b[4];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          a[i][0] = As[stage][kk + t4][wm + i * 16 + g];
-          a[i][1] = As[stage][kk + t4][wm + i * 16 + g + 8];
+          a[i][0] = a_at(stage, kk + t4, wm + i * 16 + g);
+          a[i][1] = a_at(stage, kk + t4, wm + i * 16 + g + 8);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[stage][kk + t4][wn + j * 8 + g];
+        for (int j = 0; j < 4; ++j) b[j] = b_at(stage, kk + t4, wn + j * 8 + g);
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -161,14 +171,14 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const cplx x0 = As[stage][kk + t4][wm + i * 16 + g];
-          const cplx x1 = As[stage][kk + t4][wm + i * 16 + g + 8];
+          const cplx x0 = a_at(stage, kk + t4, wm + i * 16 + g);
+          const cplx x1 = a_at(stage, kk + t4, wm + i * 16 + g + 8);
           ar[i][0] = x0.x; ai[i][0] = sa * x0.y; nai[i][0] = -ai[i][0];
           ar[i][1] = x1.x; ai[i][1] = sa * x1.y; nai[i][1] = -ai[i][1];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const cplx y = Bs[stage][kk + t4][wn + j * 8 + g];
+          const cplx y = b_at(stage, kk + t4, wn + j * 8 + g);
           br[j] = y.x; bi[j] = sb * y.y;
         }
 #pragma unroll
