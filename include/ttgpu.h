@@ -146,6 +146,18 @@ ttg_status ttg_apply(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, const 
 /* mps.hpp:310-313 canonicalize(MPS, centre, Strategy) (QR pass + truncating sweep). */
 ttg_status ttg_canonicalize(ttg_ctx* ctx, const ttg_dmps* v, int center, const ttg_strategy* strategy,
                             ttg_dmps** out, ttg_report* reports);
+/* mps.hpp:326-405 MPSSum(weights, states).join(): block-diagonal concatenation of the scaled
+ * single-chain states (MPS::scaled semantics, mps.hpp:98-117); nterms = 1 gives states[0].scaled(w).
+ * error = sum |w_l| err_l.  With the variational simplify this is combine / simplify(MPSSum)
+ * (simplify.hpp:151-215). w_im may be NULL. */
+ttg_status ttg_mps_join(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
+                        const ttg_dmps* const* states, ttg_dmps** out);
+/* simplify.hpp:151-215 simplify(MPSSum, strategy, guess) == combine(weights, states, strategy):
+ * closest MPS under `strategy` to sum_l w_l states[l] (single chains).  guess NULL = default_guess
+ * (largest |w_l| |states[l]|, scaled).  One report. */
+ttg_status ttg_simplify_sum(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
+                            const ttg_dmps* const* states, const ttg_strategy* strategy, const ttg_dmps* guess,
+                            ttg_dmps** out, ttg_report* report);
 /* mps.hpp:416-423 scprod(u, v) per chain: out_re/out_im[count]. */
 ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double* out_re, double* out_im);
 

@@ -1,6 +1,6 @@
 // Drop-in ttlab/blas.hpp hot-path entries on the B200:
-// apply(MPO, MPS, Strategy) (/root/reference/proj/include/ttlab/blas.hpp:8-11) and
-// hadamard(MPS, MPS) (:45-67).
+// apply(MPO, MPS, Strategy) (/root/reference/proj/include/ttlab/blas.hpp:8-11), apply(MPO, MPSSum)
+// (:13-20), apply(MPOList, MPS | MPSSum) (:24-42) and hadamard(MPS, MPS) (:45-67).
 #pragma once
 
 #include "ttlab/simplify.hpp"
@@ -16,6 +16,27 @@ inline CanonicalMPS apply(const MPO& op, const MPS& v, const Strategy& strategy 
   gpu::check(gpu::ctx(), ttg_apply(gpu::ctx(), w.h, d.h, &s, &out, nullptr));
   gpu::DMps o(out);
   return gpu::canonical_from(o.h, 0);
+}
+
+inline CanonicalMPS apply(const MPO& op, const MPSSum& v, const Strategy& strategy = DEFAULT_STRATEGY) {
+  std::vector<MPS> applied;
+  applied.reserve(static_cast<size_t>(v.terms()));
+  for (const auto& s : v.states()) applied.push_back(detail::apply_raw(op, s));
+  return simplify(MPSSum(v.weights(), applied), strategy);
+}
+
+inline CanonicalMPS apply(const MPOList& ops, const MPS& v, const Strategy& strategy = DEFAULT_STRATEGY) {
+  if (ops.terms() == 0) throw shape_error("apply: empty MPO list");
+  CanonicalMPS state = apply(ops[ops.terms() - 1], v, strategy);
+  for (index_t k = ops.terms() - 2; k >= 0; --k) state = apply(ops[k], state, strategy);
+  return state;
+}
+
+inline CanonicalMPS apply(const MPOList& ops, const MPSSum& v, const Strategy& strategy = DEFAULT_STRATEGY) {
+  if (ops.terms() == 0) throw shape_error("apply: empty MPO list");
+  CanonicalMPS state = apply(ops[ops.terms() - 1], v, strategy);
+  for (index_t k = ops.terms() - 2; k >= 0; --k) state = apply(ops[k], state, strategy);
+  return state;
 }
 
 inline MPS hadamard(const MPS& u, const MPS& v) {

@@ -169,7 +169,34 @@ inline DMpo upload(const MPO& op) {
   return w;
 }
 
+/// Device handles of the summands plus the C arrays ttg_mps_join / ttg_simplify_sum take.
+struct SumArgs {
+  std::vector<DMps> states;
+  std::vector<const ttg_dmps*> handles;
+  std::vector<double> wr, wi;
+  explicit SumArgs(const MPSSum& s) {
+    states.reserve(s.states().size());
+    for (size_t l = 0; l < s.states().size(); ++l) {
+      states.push_back(upload(s.states()[l]));
+      handles.push_back(states.back().h);
+      wr.push_back(s.weights()[l].real());
+      wi.push_back(s.weights()[l].imag());
+    }
+  }
+  int n() const { return static_cast<int>(handles.size()); }
+};
+
 }  // namespace gpu
+
+inline MPS MPSSum::join() const {
+  gpu::SumArgs a(*this);
+  ttg_dmps* out = nullptr;
+  gpu::check(gpu::ctx(), ttg_mps_join(gpu::ctx(), a.n(), a.wr.data(), a.wi.data(), a.handles.data(), &out));
+  gpu::DMps o(out);
+  double err = 0.0;
+  auto ts = gpu::download(o.h, 0, &err, nullptr);
+  return MPS(std::move(ts), err);
+}
 
 // ---- hot-path entry points (definitions of the declarations in mps.hpp / mpo.hpp)
 

@@ -1,5 +1,6 @@
 // Drop-in restatement of the MPO container of ttlab/mpo.hpp
-// (/root/reference/proj/include/ttlab/mpo.hpp:14-155) and detail::apply_raw (:213-238, device).
+// (/root/reference/proj/include/ttlab/mpo.hpp:14-155), MPOList (:109-129) and
+// detail::apply_raw (:213-238, device).
 #pragma once
 
 #include <vector>
@@ -32,6 +33,25 @@ public:
 
 private:
   std::vector<Tensor4> tensors_;
+};
+
+/// Product of MPO factors; the last entry is applied first (mpo.hpp:109-129).
+class MPOList {
+public:
+  MPOList() = default;
+  explicit MPOList(std::vector<MPO> factors) : factors_(std::move(factors)) {}
+  index_t terms() const { return static_cast<index_t>(factors_.size()); }
+  const MPO& operator[](index_t k) const { return factors_[static_cast<size_t>(k)]; }
+  const std::vector<MPO>& factors() const { return factors_; }
+  void push_back(MPO op) { factors_.push_back(std::move(op)); }
+  MPOList concatenated(const MPOList& other) const {
+    MPOList out = *this;
+    for (const auto& f : other.factors_) out.push_back(f);
+    return out;
+  }
+
+private:
+  std::vector<MPO> factors_;
 };
 
 inline MPO mpo_identity(index_t L, index_t d) {

@@ -1,5 +1,5 @@
 // Drop-in restatement of the MPS containers of ttlab/mps.hpp
-// (/root/reference/proj/include/ttlab/mps.hpp:21-143, 180-323, 416-449, 493-544).
+// (/root/reference/proj/include/ttlab/mps.hpp:21-143, 180-323, 326-412, 416-449, 493-544).
 // Containers keep the reference's value semantics and host storage; every
 // numerical operation on the hot path (canonical form, norms, overlaps)
 // executes on the B200 through the C ABI (include/ttgpu.h, see gpu.hpp).
@@ -54,6 +54,25 @@ public:
   double update_error(double delta) { return error_ += delta; }
   double norm_squared() const;  // <v,v> on the device (gpu.hpp)
   double norm() const { return std::sqrt(std::max(0.0, norm_squared())); }
+  /// mps.hpp:98-117 (host container operation): |f|^(1/L) on every tensor, phase on the first.
+  MPS scaled(cplx factor) const {
+    const double mag = std::abs(factor);
+    if (mag == 0.0) return zero_like();
+    std::vector<Tensor3> out = tensors_;
+    const double root = std::pow(mag, 1.0 / static_cast<double>(size()));
+    const cplx phase = factor / mag;
+    for (size_t n = 0; n < out.size(); ++n) {
+      const cplx f = n == 0 ? root * phase : cplx(root);
+      for (index_t i = 0; i < out[n].size(); ++i) out[n].data()[i] *= f;
+    }
+    return MPS(std::move(out), error_ * mag);
+  }
+  /// mps.hpp:120-126
+  MPS zero_like() const {
+    std::vector<Tensor3> out;
+    for (const auto& t : tensors_) out.emplace_back(1, t.phys_dim(), 1);
+    return MPS(std::move(out), 0.0);
+  }
 
 protected:
   void check_shape() const {
@@ -91,6 +110,33 @@ private:
 inline CanonicalMPS canonicalize(const MPS& state, index_t center = 0, const Strategy& strategy = DEFAULT_STRATEGY) {
   return CanonicalMPS(state, center, strategy);
 }
+
+/// Lazy weighted sum of MPS with equal physical dimensions (mps.hpp:326-412).
+class MPSSum {
+public:
+  MPSSum(std::vector<cplx> weights, std::vector<MPS> states)
+      : weights_(std::move(weights)), states_(std::move(states)) {
+    if (weights_.empty() || weights_.size() != states_.size())
+      throw shape_error("MPSSum: weights and states must be non-empty and match");
+    const auto dims = states_.front().physical_dimensions();
+    for (const auto& s : states_)
+      if (s.physical_dimensions() != dims) throw shape_error("MPSSum: states must share physical dimensions");
+  }
+  const std::vector<cplx>& weights() const { return weights_; }
+  const std::vector<MPS>& states() const { return states_; }
+  index_t terms() const { return static_cast<index_t>(states_.size()); }
+  index_t size() const { return states_.front().size(); }
+  double error() const {  // mps.hpp:344-349
+    double acc = 0.0;
+    for (size_t l = 0; l < states_.size(); ++l) acc += std::abs(weights_[l]) * states_[l].error();
+    return acc;
+  }
+  MPS join() const;  // mps.hpp:352-405 (device block concatenation, gpu.hpp)
+
+private:
+  std::vector<cplx> weights_;
+  std::vector<MPS> states_;
+};
 
 cplx scprod(const MPS& u, const MPS& v);  // mps.hpp:416-423 (device)
 inline double norm(const MPS& s) { return s.norm(); }

@@ -569,19 +569,113 @@ def simplify(target: MPS, strategy: Strategy = DEFAULT_STRATEGY, guess: Optional
     return res.state
 
 
-def combine(weights, states, strategy=DEFAULT_STRATEGY):
-    """simplify.hpp:151-179 (used only by the pins; §8f 'next')."""
-    if not weights or len(weights) != len(states):
-        raise ShapeError("combine: weights and states must be non-empty and match")
-    carried = sum(abs(w) * s.error for w, s in zip(weights, states))
+class MPSSum:
+    """mps.hpp:326-412: lazy weighted sum of states with equal physical dimensions."""
+
+    def __init__(self, weights, states):
+        weights, states = list(weights), list(states)
+        if not weights or len(weights) != len(states):
+            raise ShapeError("MPSSum: weights and states must be non-empty and match")
+        dims = states[0].physical_dimensions()
+        for st in states:
+            if st.physical_dimensions() != dims:
+                raise ShapeError("MPSSum: states must share physical dimensions")
+        self.weights, self.states = weights, states
+
+    def error(self) -> float:  # mps.hpp:344-349
+        return float(sum(abs(w) * st.error for w, st in zip(self.weights, self.states)))
+
+    def join(self) -> MPS:  # mps.hpp:352-405
+        scaled = [st.scaled(w) for w, st in zip(self.weights, self.states)]
+        if len(scaled) == 1:
+            return scaled[0]
+        L = len(scaled[0])
+        cplx = any(np.iscomplexobj(t) for sc in scaled for t in sc.tensors)
+        dt = np.complex128 if cplx else np.float64
+        out = []
+        for n in range(L):
+            dl = sum(sc[n].shape[0] for sc in scaled)
+            dr = sum(sc[n].shape[2] for sc in scaled)
+            d = scaled[0][n].shape[1]
+            if n == 0:
+                t = np.zeros((1, d, dr), dtype=dt)
+                off = 0
+                for sc in scaled:
+                    b = sc[n].shape[2]
+                    t[0, :, off:off + b] = sc[n][0]
+                    off += b
+            elif n == L - 1:
+                t = np.zeros((dl, d, 1), dtype=dt)
+                off = 0
+                for sc in scaled:
+                    a = sc[n].shape[0]
+                    t[off:off + a, :, 0] = sc[n][:, :, 0]
+                    off += a
+            else:
+                t = np.zeros((dl, d, dr), dtype=dt)
+                ol = orr = 0
+                for sc in scaled:
+                    a, _, b = sc[n].shape
+                    t[ol:ol + a, :, orr:orr + b] = sc[n]
+                    ol += a
+                    orr += b
+            out.append(t)
+        return MPS(out, self.error())
+
+
+def default_guess(weights, states) -> MPS:
+    """simplify.hpp:133-144."""
     best, bw = 0, -1.0
-    for l, s in enumerate(states):  # simplify.hpp:133-144
-        w = abs(weights[l]) * s.norm()
+    for l, st in enumerate(states):
+        w = abs(weights[l]) * st.norm()
         if w > bw:
             best, bw = l, w
-    res = variational_compress(weights, states, states[best].scaled(weights[best]), strategy)
+    return states[best].scaled(weights[best])
+
+
+def simplify_sum(target: MPSSum, strategy: Strategy = DEFAULT_STRATEGY, guess: Optional[MPS] = None,
+                 report: Optional[dict] = None) -> CanonicalMPS:
+    """simplify.hpp:198-215 (simplify(MPSSum))."""
+    if strategy.method == SVD_TRUNCATE:
+        out = CanonicalMPS(target.join(), 0, strategy.with_normalize(False))
+        if strategy.normalize:
+            out.normalize_in_place()
+        return out
+    carried = target.error()
+    res = variational_compress(target.weights, target.states,
+                               guess if guess is not None else default_guess(target.weights, target.states),
+                               strategy)
     res.state.error = carried + res.residual
+    if strategy.normalize:
+        res.state.normalize_in_place()
+    if report is not None:
+        report.update(sweeps=res.sweeps, residual=res.residual, converged=res.converged,
+                      dist2=res.dist2_history, target_norm2=res.target_norm2)
     return res.state
+
+
+def combine(weights, states, strategy=DEFAULT_STRATEGY) -> CanonicalMPS:
+    """simplify.hpp:151-179."""
+    weights, states = list(weights), list(states)
+    if not weights or len(weights) != len(states):
+        raise ShapeError("combine: weights and states must be non-empty and match")
+    dims = states[0].physical_dimensions()
+    for st in states:
+        if st.physical_dimensions() != dims:
+            raise ShapeError("combine: states must share physical dimensions")
+    carried = sum(abs(w) * st.error for w, st in zip(weights, states))
+    if strategy.method == SVD_TRUNCATE:
+        joined = MPSSum(weights, states).join()
+        out = CanonicalMPS(joined, 0, strategy.with_normalize(False))
+        out.error = out.error - joined.error
+    else:
+        res = variational_compress(weights, states, default_guess(weights, states), strategy)
+        out = res.state
+        out.error = res.residual
+    out.error = carried + out.error
+    if strategy.normalize:
+        out.normalize_in_place()
+    return out
 
 
 # ----------------------------------------------------------------------------
@@ -605,6 +699,21 @@ def apply_raw(op: MPO, v: MPS) -> MPS:
 def apply(op: MPO, v: MPS, strategy: Strategy = DEFAULT_STRATEGY, **kw) -> CanonicalMPS:
     """blas.hpp:8-11."""
     return simplify(apply_raw(op, v), strategy, **kw)
+
+
+def apply_sum(op: MPO, v: MPSSum, strategy: Strategy = DEFAULT_STRATEGY) -> CanonicalMPS:
+    """blas.hpp:13-20."""
+    return simplify_sum(MPSSum(v.weights, [apply_raw(op, st) for st in v.states]), strategy)
+
+
+def apply_list(ops: Sequence[MPO], v, strategy: Strategy = DEFAULT_STRATEGY) -> CanonicalMPS:
+    """blas.hpp:24-42: factors applied last entry first; v an MPS or an MPSSum."""
+    if len(ops) == 0:
+        raise ShapeError("apply: empty MPO list")
+    state = apply_sum(ops[-1], v, strategy) if isinstance(v, MPSSum) else apply(ops[-1], v, strategy)
+    for k in range(len(ops) - 2, -1, -1):
+        state = apply(ops[k], state, strategy)
+    return state
 
 
 def hadamard(u: MPS, v: MPS) -> MPS:

@@ -650,7 +650,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
         E.G(target.site[k], target.cap[k], xb.p, xcap, eb[(k + 1) & 1], ecap, dconst(t[k + 1]), dconst(t[k + 1]),
             dconst(t[k] * d[k]), OP_C, OP_N, false);
       }
-      CK(frob2<T>(eb[L & 1], ecap, dconst(1), dconst(1), E.d_bonds, E.ld, tn2, s_st, B, st));  // |<T,T>|
+      CK(env_real<T>(eb[L & 1], ecap, tn2, s_st, B, st));  // <T,T>
       ++ctx->launches;
     }
   }
@@ -1326,6 +1326,131 @@ ttg_status ttg_canonicalize(ttg_ctx* ctx, const ttg_dmps* v, int center, const t
     if (!v) throw Error{TTG_INVALID, "null argument"};
     if (center < 0 || center >= v->n) throw Error{TTG_SHAPE, "canonical center out of range"};  // mps.hpp:190-191
     dispatch_simplify(ctx, v, nullptr, *strategy, false, center, out, reports);
+  });
+}
+
+// MPSSum::join (mps.hpp:352-405).  sum_single: for a one-site chain the terms are
+// added into one 1 x d x 1 tensor (the L == 1 branch of CompressionEngine::sweep,
+// simplify.hpp:62-70) instead of being rejected.
+static ttg_dmps* join_states(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
+                             const ttg_dmps* const* states, bool sum_single) {
+    if (nterms < 1 || !w_re || !states) throw Error{TTG_SHAPE, "MPSSum: weights and states must be non-empty and match"};
+    const ttg_dmps* s0 = states[0];
+    if (!s0) throw Error{TTG_INVALID, "null state"};
+    const int n = s0->n;
+    bool cplx_out = false;
+    for (int l = 0; l < nterms; ++l) {
+      const ttg_dmps* st = states[l];
+      if (!st || st->count != 1) throw Error{TTG_INVALID, "join takes single chains"};
+      if (st->n != n) throw Error{TTG_SHAPE, "MPSSum: states must share physical dimensions"};
+      for (int k = 0; k < n; ++k)
+        if (st->phys[k] != s0->phys[k]) throw Error{TTG_SHAPE, "MPSSum: states must share physical dimensions"};
+      cplx_out = cplx_out || st->dtype == TTG_C128 || (w_im && w_im[l] != 0.0) ;
+    }
+    if (n == 1 && nterms > 1 && !sum_single) throw Error{TTG_SHAPE, "MPS boundary bonds must have size one"};
+    const int dtype = cplx_out ? TTG_C128 : TTG_F64;
+    // MPS::scaled(w) (mps.hpp:98-117): |w|^(1/n) on every site, phase on site 0; w = 0 -> zero_like
+    std::vector<double> mag(nterms);
+    std::vector<std::vector<int>> bl(nterms, std::vector<int>(n + 1, 1));
+    for (int l = 0; l < nterms; ++l) {
+      mag[l] = std::hypot(w_re[l], w_im ? w_im[l] : 0.0);
+      for (int k = 0; k <= n; ++k) bl[l][k] = mag[l] == 0.0 ? 1 : states[l]->bond(0, k);
+    }
+    std::vector<int> bonds(n + 1, 0);
+    for (int k = 0; k <= n; ++k)
+      for (int l = 0; l < nterms; ++l) bonds[k] += bl[l][k];
+    bonds[0] = bonds[n] = 1;
+    if (nterms == 1 || n == 1) bonds = bl[0];
+    std::vector<long long> cap(n);
+    for (int k = 0; k < n; ++k) cap[k] = (long long)bonds[k] * s0->phys[k] * bonds[k + 1];
+    ttg_dmps* o = new_dmps(n, dtype, 1, s0->phys, cap, ctx->stream);
+    std::unique_ptr<ttg_dmps> guard(o);
+    for (int k = 0; k <= n; ++k) o->bonds[k] = bonds[k];
+    double err = 0.0;
+    for (int l = 0; l < nterms; ++l) err += mag[l] * states[l]->error[0];  // MPSSum::error (mps.hpp:344-349)
+    o->error[0] = err;
+    const size_t es = esize(dtype);
+    for (int k = 0; k < n; ++k) {
+      CK(cudaMemsetAsync(o->site[k], 0, (size_t)cap[k] * es, ctx->stream));
+      int offl = 0, offr = 0;
+      for (int l = 0; l < nterms; ++l) {
+        const ttg_dmps* st = states[l];
+        const int a = bl[l][k], b = bl[l][k + 1], d = s0->phys[k];
+        const int ol = (k == 0 || nterms == 1) ? 0 : offl, orr = (k == n - 1 || nterms == 1) ? 0 : offr;
+        if (mag[l] != 0.0) {
+          const double root = std::pow(mag[l], 1.0 / n);
+          double fr = root, fi = 0.0;
+          if (k == 0) {
+            fr = root * w_re[l] / mag[l];
+            fi = root * (w_im ? w_im[l] : 0.0) / mag[l];
+          }
+          if (dtype == TTG_F64)
+            CK((join_block<double, double>(static_cast<const double*>(st->site[k]), a, d, b,
+                                          static_cast<double*>(o->site[k]), bonds[k + 1], ol, orr, fr, fi,
+                                          ctx->stream)));
+          else if (st->dtype == TTG_F64)
+            CK((join_block<double, cplx>(static_cast<const double*>(st->site[k]), a, d, b,
+                                        static_cast<cplx*>(o->site[k]), bonds[k + 1], ol, orr, fr, fi, ctx->stream)));
+          else
+            CK((join_block<cplx, cplx>(static_cast<const cplx*>(st->site[k]), a, d, b, static_cast<cplx*>(o->site[k]),
+                                      bonds[k + 1], ol, orr, fr, fi, ctx->stream)));
+          ++ctx->launches;
+        }
+        offl += a;
+        offr += b;
+      }
+    }
+    return guard.release();
+}
+
+ttg_status ttg_mps_join(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
+                        const ttg_dmps* const* states, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!out) throw Error{TTG_INVALID, "null argument"};
+    *out = join_states(ctx, nterms, w_re, w_im, states, false);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+ttg_status ttg_simplify_sum(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
+                            const ttg_dmps* const* states, const ttg_strategy* strategy, const ttg_dmps* guess,
+                            ttg_dmps** out, ttg_report* report) {
+  return guarded(ctx, [&] {
+    check_strategy(strategy);
+    if (!out) throw Error{TTG_INVALID, "null argument"};
+    if (strategy->method == TTG_SVD_TRUNCATE) {  // simplify.hpp:200-206: canonical form of the joined tensors
+      std::unique_ptr<ttg_dmps> joined(join_states(ctx, nterms, w_re, w_im, states, false));
+      dispatch_simplify(ctx, joined.get(), nullptr, *strategy, false, 0, out, report);
+      return;
+    }
+    // Variational (simplify.hpp:207-214).  The summand environments of
+    // CompressionEngine are the diagonal blocks of the joined target's
+    // environments, so the sweep runs on the joined tensors; <T,T> comes from the
+    // env chain of the join (= sum_lm conj(w_l) w_m <T_l,T_m>, simplify.hpp:37-41).
+    std::unique_ptr<ttg_dmps> joined(join_states(ctx, nterms, w_re, w_im, states, true));
+    std::unique_ptr<ttg_dmps> def_guess;
+    const ttg_dmps* G = guess;
+    if (joined->n == 1) {
+      G = nullptr;  // one-site chains: the summed tensor itself (simplify.hpp:62-70)
+    } else if (!G) {
+      // default_guess (simplify.hpp:132-143): the term with the largest |w_l| |T_l|, scaled by w_l
+      int best = 0;
+      double best_w = -1.0;
+      for (int l = 0; l < nterms; ++l) {
+        double re = 0.0, im = 0.0;
+        const ttg_status st = ttg_scprod(ctx, states[l], states[l], &re, &im);
+        if (st != TTG_OK) throw Error{st, ttg_last_error(ctx)};
+        const double w = std::hypot(w_re[l], w_im ? w_im[l] : 0.0) * std::sqrt(std::max(0.0, re));
+        if (w > best_w) {
+          best_w = w;
+          best = l;
+        }
+      }
+      const double wi = w_im ? w_im[best] : 0.0;
+      def_guess.reset(join_states(ctx, 1, &w_re[best], &wi, &states[best], false));
+      G = def_guess.get();
+    }
+    dispatch_simplify(ctx, joined.get(), G, *strategy, true, 0, out, report);
   });
 }
 

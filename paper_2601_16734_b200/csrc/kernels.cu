@@ -185,6 +185,42 @@ __global__ void copy_bond_kernel(int* bonds, int ld, int from, int to, int chain
   if (c < chains) bonds[c * ld + to] = bonds[c * ld + from];
 }
 
+template <typename TS, typename TD>
+__global__ void join_block_kernel(const TS* src, int a_dim, int d, int b_dim, TD* dst, int dst_right, int offl, int offr,
+                                  double f_re, double f_im) {
+  const long long total = (long long)a_dim * d * b_dim;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx % b_dim);
+    const long long as = idx / b_dim;
+    const int sp = (int)(as % d), a = (int)(as / d);
+    TD* o = dst + ((long long)(offl + a) * d + sp) * dst_right + offr + b;
+    if constexpr (Scalar<TD>::is_complex) {
+      cplx x;
+      if constexpr (Scalar<TS>::is_complex)
+        x = src[idx];
+      else
+        x = cplx{src[idx], 0.0};
+      const cplx y = *o;  // accumulate: blocks are disjoint except for the summed one-site case
+      *o = cplx{y.x + f_re * x.x - f_im * x.y, y.y + f_re * x.y + f_im * x.x};
+    } else {
+      *o += f_re * src[idx];
+    }
+  }
+}
+
+template <typename T>
+__global__ void env_real_kernel(const T* X, long long sX, double* out, long long s_out, int chains) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= chains) return;
+  double v;
+  if constexpr (Scalar<T>::is_complex)
+    v = X[c * sX].x;
+  else
+    v = X[c * sX];
+  out[c * s_out] = v > 0.0 ? v : 0.0;
+}
+
 int grid_for(long long total, int threads) {
   long long b = (total + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -255,6 +291,29 @@ cudaError_t init_state(ChainState* st, int chains, cudaStream_t s) {
   init_state_kernel<<<(chains + 255) / 256, 256, 0, s>>>(st, chains);
   return cudaGetLastError();
 }
+
+template <typename TS, typename TD>
+cudaError_t join_block(const TS* src, int a_dim, int d, int b_dim, TD* dst, int dst_right, int offl, int offr,
+                       double f_re, double f_im, cudaStream_t s) {
+  const long long total = (long long)a_dim * d * b_dim;
+  join_block_kernel<TS, TD><<<grid_for(total, 256), 256, 0, s>>>(src, a_dim, d, b_dim, dst, dst_right, offl, offr,
+                                                                 f_re, f_im);
+  return cudaGetLastError();
+}
+template cudaError_t join_block<double, double>(const double*, int, int, int, double*, int, int, int, double, double,
+                                                cudaStream_t);
+template cudaError_t join_block<double, cplx>(const double*, int, int, int, cplx*, int, int, int, double, double,
+                                              cudaStream_t);
+template cudaError_t join_block<cplx, cplx>(const cplx*, int, int, int, cplx*, int, int, int, double, double,
+                                            cudaStream_t);
+
+template <typename T>
+cudaError_t env_real(const T* X, long long sX, double* out, long long s_out, int chains, cudaStream_t s) {
+  env_real_kernel<T><<<(chains + 127) / 128, 128, 0, s>>>(X, sX, out, s_out, chains);
+  return cudaGetLastError();
+}
+template cudaError_t env_real<double>(const double*, long long, double*, long long, int, cudaStream_t);
+template cudaError_t env_real<cplx>(const cplx*, long long, double*, long long, int, cudaStream_t);
 
 cudaError_t begin_sweeps(ChainState* st, int chains, cudaStream_t s) {
   begin_sweeps_kernel<<<(chains + 255) / 256, 256, 0, s>>>(st, chains);

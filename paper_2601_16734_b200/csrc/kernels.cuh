@@ -21,6 +21,10 @@ template <typename T>
 cudaError_t frob2(const T* X, long long sX, DimExpr rows, DimExpr cols, const int* bonds, int ld, double* out,
                   long long s_out, int chains, cudaStream_t s);
 
+// out[c * s_out] = max(0, Re X_c[0]) (a closed <T,T> environment chain, simplify.hpp:37-41)
+template <typename T>
+cudaError_t env_real(const T* X, long long sX, double* out, long long s_out, int chains, cudaStream_t s);
+
 // End of a variational sweep (simplify.hpp:90, 114-125): dist2 from the
 // centre tensor psi_0 (size elems), convergence + plateau rules.
 template <typename T>
@@ -37,6 +41,12 @@ template <typename T>
 cudaError_t fill_one(T* dst, long long s_dst, int chains, cudaStream_t s);
 
 cudaError_t real_to_complex(const double* src, cplx* dst, long long n, cudaStream_t s);
+
+// MPSSum::join block (mps.hpp:352-405): dst[offl + a, s, offr + b] += f * src[a, s, b]
+// for a src tensor (a_dim x d x b_dim) inside dst (. x d x dst_right).
+template <typename TS, typename TD>
+cudaError_t join_block(const TS* src, int a_dim, int d, int b_dim, TD* dst, int dst_right, int offl, int offr,
+                       double f_re, double f_im, cudaStream_t s);
 
 // gather per-chain device tensors into one packed site buffer
 template <typename T>

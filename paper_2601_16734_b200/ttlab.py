@@ -4,7 +4,9 @@ Names, argument meaning and error behaviour follow `ttlab`
 (/root/reference/proj/include/ttlab/): `Strategy` (types.hpp:50-94),
 `apply` (blas.hpp:8-11), `hadamard` (blas.hpp:45-67), `simplify`
 (simplify.hpp:182-195), `canonicalize` (mps.hpp:310-313), `scprod`
-(mps.hpp:416-423), `detail::apply_raw` (mpo.hpp:213-238).  Every operation
+(mps.hpp:416-423), `detail::apply_raw` (mpo.hpp:213-238), `MPSSum` /
+`combine` / `simplify(MPSSum)` (mps.hpp:326-405, simplify.hpp:151-215) and
+`MPOList` with `apply(MPOList, ...)` (mpo.hpp:109-129, blas.hpp:13-42).  Every operation
 runs through the C ABI of `libttgpu.so`; there is no CPU path.
 
 States are `DeviceMPS` handles (device resident, optionally a batch of
@@ -100,6 +102,18 @@ class Context:
             raise DeviceError(f"ttg_create(device={device}) failed with status {st}: no usable CUDA device")
         self.handle = h
         self.device = device
+        # device objects allocated on this context's stream: freed before the
+        # stream goes away even when the garbage collector finalises the
+        # context first (reference cycles at interpreter exit)
+        self._live = {}
+
+    def _track(self, handle: C.c_void_p, free):
+        self._live[handle.value] = free
+
+    def _release(self, handle: C.c_void_p):
+        free = self._live.pop(handle.value, None) if handle and self._live is not None else None
+        if free is not None:
+            free(handle)
 
     def check(self, status: int):
         if status != _lib.TTG_OK:
@@ -134,8 +148,12 @@ class Context:
 
     def __del__(self):
         try:
+            live, self._live = self._live, None
+            for hv, free in (live or {}).items():
+                free(C.c_void_p(hv))
             if self.handle:
                 lib.ttg_destroy(self.handle)
+                self.handle = None
         except Exception:
             pass
 
@@ -170,6 +188,7 @@ class DeviceMPS:
     def __init__(self, handle: C.c_void_p, ctx: Context):
         self.handle = handle
         self.ctx = ctx
+        ctx._track(handle, lib.ttg_mps_free)
 
     # ---- construction
     @classmethod
@@ -215,7 +234,7 @@ class DeviceMPS:
     def __del__(self):
         try:
             if self.handle:
-                lib.ttg_mps_free(self.handle)
+                self.ctx._release(self.handle)
                 self.handle = None
         except Exception:
             pass
@@ -289,11 +308,12 @@ class DeviceMPO:
         h = C.c_void_p()
         ctx.check(lib.ttg_mpo_upload(ctx.handle, C.byref(view), C.byref(h)))
         self.handle, self.ctx = h, ctx
+        ctx._track(h, lib.ttg_mpo_free)
 
     def __del__(self):
         try:
             if self.handle:
-                lib.ttg_mpo_free(self.handle)
+                self.ctx._release(self.handle)
                 self.handle = None
         except Exception:
             pass
@@ -338,8 +358,104 @@ def hadamard(u, v) -> DeviceMPS:
     return DeviceMPS(h, u.ctx)
 
 
+class MPSSum:
+    """Lazy weighted sum of states with equal physical dimensions (mps.hpp:326-349).
+
+    The states stay device handles; `join()` materialises the block-diagonal
+    concatenation on the GPU (mps.hpp:352-405)."""
+
+    def __init__(self, weights, states, ctx: Optional[Context] = None):
+        weights = [complex(w) for w in weights]
+        states = list(states)
+        if not weights or len(weights) != len(states):
+            raise ShapeError("MPSSum: weights and states must be non-empty and match")
+        ctx = ctx or next((s.ctx for s in states if isinstance(s, DeviceMPS)), None)
+        self.states = [_as_mps(s, ctx) for s in states]
+        self.weights = weights
+        dims = self.states[0].info()["phys"]
+        for s in self.states:
+            if s.count != 1:
+                raise ShapeError("MPSSum: single-chain states only")
+            if s.info()["phys"] != dims:
+                raise ShapeError("MPSSum: states must share physical dimensions")
+
+    @property
+    def ctx(self) -> Context:
+        return self.states[0].ctx
+
+    def terms(self) -> int:
+        return len(self.states)
+
+    def __len__(self):
+        return len(self.states[0])
+
+    def error(self) -> float:
+        """mps.hpp:344-349."""
+        return float(sum(abs(w) * s.error() for w, s in zip(self.weights, self.states)))
+
+    def _c_args(self):
+        n = len(self.weights)
+        wr = (C.c_double * n)(*[w.real for w in self.weights])
+        wi = (C.c_double * n)(*[w.imag for w in self.weights])
+        hs = (C.c_void_p * n)(*[s.handle.value for s in self.states])
+        return n, wr, wi, hs
+
+    def join(self) -> DeviceMPS:
+        """mps.hpp:352-405 on the device."""
+        n, wr, wi, hs = self._c_args()
+        h = C.c_void_p()
+        self.ctx.check(lib.ttg_mps_join(self.ctx.handle, n, wr, wi, hs, C.byref(h)))
+        return DeviceMPS(h, self.ctx)
+
+
+class MPOList:
+    """Product of MPO factors, the last entry applied first (mpo.hpp:109-129)."""
+
+    def __init__(self, factors=()):
+        self.factors = list(factors)
+
+    def terms(self) -> int:
+        return len(self.factors)
+
+    def __getitem__(self, k):
+        return self.factors[k]
+
+    def push_back(self, op):
+        self.factors.append(op)
+
+    def concatenated(self, other: "MPOList") -> "MPOList":
+        return MPOList(self.factors + other.factors)
+
+
+def _simplify_sum(target: MPSSum, strategy: Strategy, guess, report) -> DeviceMPS:
+    g = None if guess is None else _as_mps(guess, target.ctx)
+    n, wr, wi, hs = target._c_args()
+    reps = _reports(1)
+    h = C.c_void_p()
+    target.ctx.check(lib.ttg_simplify_sum(target.ctx.handle, n, wr, wi, hs, C.byref(strategy._c()),
+                                          None if g is None else g.handle, C.byref(h), reps))
+    if report is not None:
+        report.extend(_report_dicts(reps, 1))
+    return DeviceMPS(h, target.ctx)
+
+
+def combine(weights, states, strategy: Strategy = DEFAULT_STRATEGY, report: Optional[list] = None) -> DeviceMPS:
+    """simplify.hpp:151-180: closest MPS under `strategy` to sum_l weights[l] states[l]."""
+    weights, states = list(weights), list(states)
+    if not weights or len(weights) != len(states):
+        raise ShapeError("combine: weights and states must be non-empty and match")
+    try:
+        target = MPSSum(weights, states)
+    except ShapeError as e:
+        raise ShapeError(str(e).replace("MPSSum", "combine")) from None
+    return _simplify_sum(target, strategy, None, report)
+
+
 def simplify(target, strategy: Strategy = DEFAULT_STRATEGY, guess=None, report: Optional[list] = None) -> DeviceMPS:
-    """simplify.hpp:182-195 (also the batched simplify when `target` is a batch)."""
+    """simplify.hpp:182-195 (also the batched simplify when `target` is a batch);
+    simplify.hpp:197-215 when `target` is an `MPSSum`."""
+    if isinstance(target, MPSSum):
+        return _simplify_sum(target, strategy, guess, report)
     t = _as_mps(target)
     g = None if guess is None else _as_mps(guess, t.ctx)
     cnt = t.count
@@ -353,7 +469,19 @@ def simplify(target, strategy: Strategy = DEFAULT_STRATEGY, guess=None, report: 
 
 
 def apply(op, v, strategy: Strategy = DEFAULT_STRATEGY, report: Optional[list] = None) -> DeviceMPS:
-    """blas.hpp:8-11."""
+    """blas.hpp:8-42: MPO or MPOList onto an MPS (or batch) or an MPSSum."""
+    if isinstance(op, MPOList):
+        if op.terms() == 0:
+            raise ShapeError("apply: empty MPO list")
+        last = op.terms() - 1
+        state = apply(op[last], v, strategy, report if last == 0 else None)
+        for k in range(last - 1, -1, -1):  # report: the final (outermost) factor
+            state = apply(op[k], state, strategy, report if k == 0 else None)
+        return state
+    if isinstance(v, MPSSum):
+        dop = _as_mpo(op, v.ctx)
+        applied = [apply_raw(dop, s) for s in v.states]
+        return _simplify_sum(MPSSum(v.weights, applied), strategy, None, report)
     v = _as_mps(v)
     op = _as_mpo(op, v.ctx)
     cnt = v.count

@@ -125,6 +125,81 @@ int main() {
       CHECK(std::abs(batch[i].error() - one.error()) < 1e-12);
     }
   });
+  section("combine: v+v, v-v, 3-term dense sum, SVD route, errors (test_blas.cpp:8-36)", [] {
+    MPS v = random_uniform_mps(4, 2, 2, 1);
+    auto s = combine({1.0, 1.0}, {v, v});
+    auto dv = mps_to_dense(v);
+    for (auto& x : dv) x *= 2.0;
+    CHECK(dist(mps_to_dense(s), dv) < 1e-12);
+    MPS u = random_uniform_mps(4, 2, 2, 2);
+    CHECK(combine({1.0, -1.0}, {u, u}).norm() <= 1e-12);
+    std::vector<MPS> states = {random_uniform_mps(5, 2, 2, 3), random_uniform_mps(5, 2, 3, 4),
+                               random_uniform_mps(5, 2, 2, 5)};
+    std::vector<cplx> w = {cplx(0.3, -1.0), cplx(-2.0, 0.1), cplx(0.0, 0.7)};
+    std::vector<cplx> expected(32, cplx(0));
+    for (size_t l = 0; l < states.size(); ++l) {
+      auto d = mps_to_dense(states[l]);
+      for (size_t i = 0; i < d.size(); ++i) expected[i] += w[l] * d[i];
+    }
+    auto sum = combine(w, states, DEFAULT_STRATEGY.with_max_sweeps(8));
+    CHECK(dist(mps_to_dense(sum), expected) < 1e-10);
+    CHECK(dist(mps_to_dense(sum), expected) <= sum.error());
+    auto svd_sum = combine(w, states, NO_TRUNCATION);
+    CHECK(dist(mps_to_dense(svd_sum), expected) < 1e-10);
+    CHECK(dist(mps_to_dense(MPSSum(w, states).join()), expected) < 1e-12);
+    bool threw = false;
+    try {
+      combine({}, {});
+    } catch (const shape_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      combine({1.0}, {random_uniform_mps(3, 2, 1, 1), random_uniform_mps(3, 2, 1, 2)});
+    } catch (const shape_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  });
+  section("simplify(MPSSum): v - v collapses to zero (test_blas.cpp:67-71)", [] {
+    MPS v = random_uniform_mps(4, 2, 3, 9);
+    auto s = simplify(MPSSum({1.0, -1.0}, {v, v}));
+    CHECK(s.norm() <= 1e-12);
+  });
+  section("apply(MPOList) right to left, apply(MPO, MPSSum) (test_blas.cpp:132-141)", [] {
+    auto local = [](cplx a, cplx b, cplx c, cplx d) {
+      std::vector<Tensor4> ts;
+      for (int n = 0; n < 3; ++n) {
+        Tensor4 t(1, 2, 2, 1);
+        if (n == 0) {
+          t(0, 0, 0, 0) = a; t(0, 0, 1, 0) = b; t(0, 1, 0, 0) = c; t(0, 1, 1, 0) = d;
+        } else {
+          t(0, 0, 0, 0) = 1.0; t(0, 1, 1, 0) = 1.0;
+        }
+        ts.push_back(std::move(t));
+      }
+      return MPO(std::move(ts));
+    };
+    const cplx m1[4] = {0.3, -1.2, 0.7, 0.4}, m2[4] = {cplx(0.1, 1.0), 0.5, -0.8, 2.0};
+    MPO a = local(m1[0], m1[1], m1[2], m1[3]), b = local(m2[0], m2[1], m2[2], m2[3]);
+    MPS v = random_uniform_mps(3, 2, 2, 13);
+    auto dv = mps_to_dense(v);  // index = s0 * 4 + rest: the local operator acts on s0
+    auto act = [](const cplx* m, const std::vector<cplx>& x) {
+      std::vector<cplx> y(x.size());
+      for (size_t r = 0; r < 4; ++r)
+        for (int j = 0; j < 2; ++j) y[j * 4 + r] = m[j * 2 + 0] * x[r] + m[j * 2 + 1] * x[4 + r];
+      return y;
+    };
+    auto expected = act(m1, act(m2, dv));
+    CHECK(dist(mps_to_dense(apply(MPOList({a, b}), v)), expected) < 1e-10);
+    MPS u = random_uniform_mps(3, 2, 2, 14);
+    auto du = mps_to_dense(u);
+    std::vector<cplx> mix(dv.size());
+    for (size_t i = 0; i < dv.size(); ++i) mix[i] = 0.5 * dv[i] + cplx(0, -1) * du[i];
+    auto got = apply(b, MPSSum({0.5, cplx(0, -1)}, {v, u}), DEFAULT_STRATEGY.with_max_sweeps(8));
+    CHECK(dist(mps_to_dense(got), act(m2, mix)) < 1e-10 * nrm(mix) + 1e-12);
+  });
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -171,8 +171,19 @@ def test_simplify_guess_accepted():
     """test_blas.cpp:72-76."""
     t = T()
     v = O.random_uniform_mps(5, 2, 3, 10)
-    s = t.simplify(v.tensors, t.DEFAULT_STRATEGY.with_max_sweeps(8), O.basis_state(5, 2, 0).tensors)
+    rep = []
+    s = t.simplify(v.tensors, t.DEFAULT_STRATEGY.with_max_sweeps(8), O.basis_state(5, 2, 0).tensors, report=rep)
     assert np.linalg.norm(dense(s.to_tensors()) - O.mps_to_dense(v)) < 1e-9 * v.norm()
+    # with a guess <T,T> comes from the environment chain (simplify.hpp:37-41), not the QR pass
+    assert abs(rep[0]["target_norm2"] - v.norm_squared()) <= 1e-12 * v.norm_squared()
+    orep = {}
+    O.simplify(v, O.DEFAULT_STRATEGY.with_max_sweeps(8), O.basis_state(5, 2, 0), report=orep)
+    # exact-rank target: after sweep 1 dist2 = <T,T> - |psi|^2 is pure rounding
+    # (~eps <T,T>), so whether the 1e-12 stop rule fires then or one sweep later
+    # depends on the last bits; sqrt(dist2) makes the residual ~sqrt(eps)|T|.
+    k = rep[0]["sweeps"]
+    assert k == orep["sweeps"] or orep["dist2"][k - 1] <= 64 * np.finfo(float).eps * v.norm_squared()
+    assert abs(rep[0]["residual"] - orep["residual"]) <= 1e-7 * v.norm()
 
 
 def test_apply_dense_oracle():

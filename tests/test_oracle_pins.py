@@ -142,6 +142,41 @@ def test_simplify_pins():
     assert O.combine([1.0, -1.0], [v, v]).norm() <= 1e-12
 
 
+def test_combine_pins():
+    """test_blas.cpp:8-36 (combine), 67-71 (simplify(MPSSum)), 132-141 (MPOList)."""
+    v = O.random_uniform_mps(4, 2, 2, 1)
+    s = O.combine([1.0, 1.0], [v, v])
+    assert np.abs(O.mps_to_dense(s) - 2.0 * O.mps_to_dense(v)).max() < 1e-12
+    v = O.random_uniform_mps(4, 2, 2, 2)
+    assert O.combine([1.0, -1.0], [v, v]).norm() <= 1e-12
+    states = [O.random_uniform_mps(5, 2, 2, 3), O.random_uniform_mps(5, 2, 3, 4), O.random_uniform_mps(5, 2, 2, 5)]
+    w = [0.3 - 1.0j, -2.0 + 0.1j, 0.7j]
+    e = sum(wl * O.mps_to_dense(st) for wl, st in zip(w, states))
+    s = O.combine(w, states, O.DEFAULT_STRATEGY.with_max_sweeps(8))
+    assert np.linalg.norm(O.mps_to_dense(s) - e) < 1e-10
+    assert np.linalg.norm(O.mps_to_dense(s) - e) <= s.error
+    s = O.combine(w, states, O.NO_TRUNCATION)
+    assert np.linalg.norm(O.mps_to_dense(s) - e) < 1e-10
+    with pytest.raises(O.ShapeError):
+        O.combine([], [])
+    with pytest.raises(O.ShapeError):
+        O.combine([1.0], [O.random_uniform_mps(3, 2, 1, 1), O.random_uniform_mps(3, 2, 1, 2)])
+    v = O.random_uniform_mps(4, 2, 3, 9)
+    assert O.simplify_sum(O.MPSSum([1.0, -1.0], [v, v])).norm() <= 1e-12
+    # join is the exact block concatenation (mps.hpp:352-405)
+    j = O.MPSSum(w, states).join()
+    assert np.abs(O.mps_to_dense(j) - e).max() < 1e-12
+    bsum = [sum(x) for x in zip(*[st.bond_dimensions() for st in states])]
+    assert j.bond_dimensions() == [1] + bsum[1:-1] + [1]
+    v = O.random_uniform_mps(3, 2, 2, 13)
+    m1, m2 = random_matrix(2, 2, 31), random_matrix(2, 2, 32)
+    i2 = np.eye(2)
+    a = O.mpo_from_local_operators([m1, i2, i2])
+    b = O.mpo_from_local_operators([m2, i2, i2])
+    e = O.mpo_to_dense(a) @ (O.mpo_to_dense(b) @ O.mps_to_dense(v))
+    assert np.linalg.norm(O.mps_to_dense(O.apply_list([a, b], v)) - e) < 1e-10
+
+
 def test_apply_and_hadamard_pins():
     """test_blas.cpp:108-142, 181-202."""
     v = O.random_uniform_mps(5, 2, 3, 11)
