@@ -855,3 +855,53 @@ def shift_mpo(n, m, periodic=True) -> MPO:
                     t[cout, o, i, 0 if site == n - 1 else cin] = 1.0
         ts.append(t)
     return MPO(ts)
+
+
+# ----------------------------------------------------------------------------
+# Fourier transform (qft.hpp:10-128), restated as dense circuits
+# ----------------------------------------------------------------------------
+
+
+def qft_layer_dense(L, sites, m, sign, carry_input) -> np.ndarray:
+    """qft.hpp:10-15 as a dense 2^L x 2^L matrix: Hadamard on qubit sites[m]
+    (site 0 most significant) and, for every later subset qubit sites[j],
+    the phase exp(i sign 2 pi c b_j / 2^(j-m+1)) with c the Hadamard's output
+    bit (forward layer: phases after H) or input bit (adjoint layer: phases
+    before H)."""
+    dim = 1 << L
+    bit = lambda x, q: (x >> (L - 1 - q)) & 1
+
+    def phase(c_of):
+        ph = np.ones(dim, dtype=np.complex128)
+        for x in range(dim):
+            c = c_of(x)
+            for j in range(m + 1, len(sites)):
+                ph[x] *= np.exp(1j * sign * 2.0 * np.pi * c * bit(x, sites[j]) / 2.0 ** (j - m + 1))
+        return np.diag(ph)
+
+    h = np.array([[1.0, 1.0], [1.0, -1.0]]) / np.sqrt(2.0)
+    q = sites[m]
+    H = np.kron(np.kron(np.eye(1 << q), h), np.eye(1 << (L - 1 - q)))
+    P = phase(lambda x: bit(x, q))
+    return H @ P if carry_input else P @ H
+
+
+def qft_dense(L, inverse=False, sites=None) -> np.ndarray:
+    """qft.hpp:67-101: product of the layers (forward: layer 0 acts first;
+    inverse: the conjugated layers in the opposite order)."""
+    subset = list(range(L)) if sites is None else list(sites)
+    sign = 1.0 if inverse else -1.0
+    order = range(len(subset) - 1, -1, -1) if inverse else range(len(subset))
+    U = np.eye(1 << L, dtype=np.complex128)
+    for m in order:
+        U = qft_layer_dense(L, subset, m, sign, inverse) @ U
+    return U
+
+
+def bit_reversal(L) -> np.ndarray:
+    """qft.hpp:114-126 (qft_flip) as a permutation matrix."""
+    dim = 1 << L
+    P = np.zeros((dim, dim))
+    for x in range(dim):
+        P[int(format(x, f"0{L}b")[::-1], 2), x] = 1.0
+    return P

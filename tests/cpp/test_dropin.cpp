@@ -7,6 +7,7 @@
 #include <string>
 
 #include "ttlab/blas.hpp"
+#include "ttlab/qft.hpp"
 
 using namespace ttlab;
 
@@ -199,6 +200,25 @@ int main() {
     for (size_t i = 0; i < dv.size(); ++i) mix[i] = 0.5 * dv[i] + cplx(0, -1) * du[i];
     auto got = apply(b, MPSSum({0.5, cplx(0, -1)}, {v, u}), DEFAULT_STRATEGY.with_max_sweeps(8));
     CHECK(dist(mps_to_dense(got), act(m2, mix)) < 1e-10 * nrm(mix) + 1e-12);
+  });
+  section("qft: e_0 -> uniform, iqft(qft(v)) = v, qft_flip(qft(v)) = DFT (test_lapack.cpp:265-291)", [] {
+    auto f = mps_to_dense(qft(basis_state(6, 2, 0)));
+    double worst = 0.0;
+    for (auto x : f) worst = std::max(worst, std::abs(x - cplx(1.0 / 8.0)));
+    CHECK(worst < 1e-12);
+    MPS v = random_uniform_mps(6, 2, 3, 23);
+    CHECK(dist(mps_to_dense(iqft(qft(v))), mps_to_dense(v)) < 1e-12 * v.norm());
+    MPS u = random_uniform_mps(6, 2, 3, 24);
+    auto x = mps_to_dense(u);
+    std::vector<cplx> expected(64);
+    const double pi = std::acos(-1.0);
+    for (int i = 0; i < 64; ++i) {
+      cplx acc(0);
+      for (int j = 0; j < 64; ++j) acc += std::polar(1.0, -2.0 * pi * i * j / 64.0) * x[static_cast<size_t>(j)];
+      expected[static_cast<size_t>(i)] = acc / 8.0;
+    }
+    CHECK(dist(mps_to_dense(qft_flip(qft(u))), expected) < 1e-10);
+    CHECK(dist(mps_to_dense(qft_flip(qft_flip(u))), x) == 0.0);
   });
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
