@@ -158,6 +158,18 @@ ttg_status ttg_mps_join(ttg_ctx* ctx, int nterms, const double* w_re, const doub
 ttg_status ttg_simplify_sum(ttg_ctx* ctx, int nterms, const double* w_re, const double* w_im,
                             const ttg_dmps* const* states, const ttg_strategy* strategy, const ttg_dmps* guess,
                             ttg_dmps** out, ttg_report* report);
+/* TTLAB1 container on the device boundary (serialize.hpp:61-121).  Files hold complex128;
+ * real_if_possible = 1 stores the loaded object as float64 when every imaginary part is zero.
+ * Errors: unreadable / bad magic / bad version / truncated / wrong rank -> TTG_NUMERIC
+ * (numeric_error), inconsistent bonds -> TTG_SHAPE.  Saving a float64 object writes
+ * complex128 with zero imaginary parts; ttg_mps_save writes one chain of a batch. */
+ttg_status ttg_mps_load(ttg_ctx* ctx, const char* path, int real_if_possible, ttg_dmps** out);
+ttg_status ttg_mps_save(ttg_ctx* ctx, const ttg_dmps* m, int chain, const char* path);
+ttg_status ttg_mpo_load(ttg_ctx* ctx, const char* path, int real_if_possible, ttg_dmpo** out);
+ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* op, const char* path);
+/* blas.hpp:128-138 expectation_mpo(op, u, v) = <u, op v> per chain (v NULL: v = u). */
+ttg_status ttg_expectation_mpo(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* u, const ttg_dmps* v, double* out_re,
+                               double* out_im);
 /* mps.hpp:416-423 scprod(u, v) per chain: out_re/out_im[count]. */
 ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double* out_re, double* out_im);
 

@@ -1,6 +1,7 @@
 // Drop-in ttlab/blas.hpp hot-path entries on the B200:
 // apply(MPO, MPS, Strategy) (/root/reference/proj/include/ttlab/blas.hpp:8-11), apply(MPO, MPSSum)
-// (:13-20), apply(MPOList, MPS | MPSSum) (:24-42) and hadamard(MPS, MPS) (:45-67).
+// (:13-20), apply(MPOList, MPS | MPSSum) (:24-42), hadamard(MPS, MPS) (:45-67) and
+// expectation_mpo (:128-138).
 #pragma once
 
 #include "ttlab/simplify.hpp"
@@ -37,6 +38,19 @@ inline CanonicalMPS apply(const MPOList& ops, const MPSSum& v, const Strategy& s
   CanonicalMPS state = apply(ops[ops.terms() - 1], v, strategy);
   for (index_t k = ops.terms() - 2; k >= 0; --k) state = apply(ops[k], state, strategy);
   return state;
+}
+
+/// <u, op v> (blas.hpp:128-138); `v` defaults to `u`.
+inline cplx expectation_mpo(const MPO& op, const MPS& u, std::optional<MPS> v = std::nullopt) {
+  const MPS& ket = v ? *v : u;
+  if (op.size() != u.size() || ket.size() != u.size()) throw shape_error("expectation_mpo: size mismatch");
+  auto w = gpu::upload(op);
+  auto du = gpu::upload(u);
+  std::optional<gpu::DMps> dv;
+  if (v) dv.emplace(gpu::upload(*v));
+  double re = 0.0, im = 0.0;
+  gpu::check(gpu::ctx(), ttg_expectation_mpo(gpu::ctx(), w.h, du.h, dv ? dv->h : nullptr, &re, &im));
+  return cplx(re, im);
 }
 
 inline MPS hadamard(const MPS& u, const MPS& v) {

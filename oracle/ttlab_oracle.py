@@ -905,3 +905,125 @@ def bit_reversal(L) -> np.ndarray:
     for x in range(dim):
         P[int(format(x, f"0{L}b")[::-1], 2), x] = 1.0
     return P
+
+
+# ----------------------------------------------------------------------------
+# operator environments and expectation values (environments.hpp:38-89,
+# blas.hpp:100-138)
+# ----------------------------------------------------------------------------
+
+
+def update_left_op_environment(env, bra, op, ket):
+    """environments.hpp:45-63: E'[c'](a',b') = sum conj(A[a,s',a']) W[c,s',s,c'] E[c](a,b) B[b,s,b'].
+    env has shape (c, a, b)."""
+    return np.einsum("cab,axy,cxsd,bsz->dyz", env, np.conj(bra), op, ket, optimize=True)
+
+
+def expectation_mpo(op: MPO, u: MPS, v: Optional[MPS] = None):
+    """blas.hpp:128-138."""
+    ket = v if v is not None else u
+    if len(op) != len(u) or len(ket) != len(u):
+        raise ShapeError("expectation_mpo: size mismatch")
+    env = np.ones((1, 1, 1), dtype=np.complex128)
+    for n in range(len(u)):
+        env = update_left_op_environment(env, u[n], op[n], ket[n])
+    if env.shape[0] != 1:
+        raise ShapeError("expectation_mpo: unclosed MPO bond")
+    return complex(env[0, 0, 0])
+
+
+def expectation_local(v: MPS, op, site, op2=None, site2=None):
+    """blas.hpp:100-125: <v, O_site v> or <v, O_site O2_site2 v> (bra/ket environment chain)."""
+    if site < 0 or site >= len(v):
+        raise ShapeError("expectation_local: site out of range")
+    if (op2 is None) != (site2 is None):
+        raise ShapeError("expectation_local: two-point value needs both operator and site")
+    if op2 is not None and (site2 < 0 or site2 >= len(v) or site2 == site):
+        raise ShapeError("expectation_local: second site out of range")
+    env = np.ones((1, 1), dtype=np.complex128)
+    for n in range(len(v)):
+        ket = v[n]
+        for o, k in ((op, site), (op2, site2)):
+            if o is not None and n == k and np.shape(o) != (ket.shape[1], ket.shape[1]):
+                raise ShapeError("local operator dimension mismatch")  # blas.hpp:88-89
+        if n == site:
+            ket = np.einsum("ts,asb->atb", op, ket)
+        if op2 is not None and n == site2:
+            ket = np.einsum("ts,asb->atb", op2, ket)
+        env = update_left_environment(env, v[n], ket)
+    return complex(env[0, 0])
+
+
+# ----------------------------------------------------------------------------
+# TTLAB1 container (serialize.hpp:13-121)
+# ----------------------------------------------------------------------------
+
+TTLAB_MAGIC = b"TTLAB1\0"
+
+
+def _write_tensor(buf: list, t: np.ndarray):
+    import struct
+    buf.append(struct.pack("<B", t.ndim) + struct.pack("<" + "Q" * t.ndim, *t.shape))
+    buf.append(np.ascontiguousarray(t, dtype="<c16").tobytes())
+
+
+def dumps_mps(state: MPS) -> bytes:
+    """serialize.hpp:67-80."""
+    import struct
+    buf = [TTLAB_MAGIC, struct.pack("<II", 1, len(state))]
+    for t in state.tensors:
+        _write_tensor(buf, t)
+    buf.append(struct.pack("<d", state.error))
+    return b"".join(buf)
+
+
+def dumps_mpo(op: MPO) -> bytes:
+    """serialize.hpp:101-112."""
+    import struct
+    buf = [TTLAB_MAGIC, struct.pack("<II", 1, len(op))]
+    for t in op.tensors:
+        _write_tensor(buf, t)
+    return b"".join(buf)
+
+
+def _reader(data: bytes):
+    import struct
+    pos = [0]
+
+    def take(n):
+        if pos[0] + n > len(data):
+            raise NumericError("ttlab container: truncated file")
+        out = data[pos[0]:pos[0] + n]
+        pos[0] += n
+        return out
+
+    def header():
+        if take(7) != TTLAB_MAGIC:
+            raise NumericError("ttlab container: bad magic")
+        version, count = struct.unpack("<II", take(8))
+        if version != 1:
+            raise NumericError("ttlab container: unsupported version")
+        return count
+
+    def tensor(rank):
+        if struct.unpack("<B", take(1))[0] != rank:
+            raise NumericError(f"ttlab container: expected rank-{rank} tensor")
+        dims = struct.unpack("<" + "Q" * rank, take(8 * rank))
+        n = int(np.prod(dims))
+        return np.frombuffer(take(16 * n), dtype="<c16").reshape(dims).astype(np.complex128)
+
+    return take, header, tensor
+
+
+def loads_mps(data: bytes) -> MPS:
+    """serialize.hpp:82-99."""
+    import struct
+    take, header, tensor = _reader(data)
+    ts = [tensor(3) for _ in range(header())]
+    return MPS(ts, struct.unpack("<d", take(8))[0])
+
+
+def loads_mpo(data: bytes) -> MPO:
+    """serialize.hpp:114-130."""
+    _, header, tensor = _reader(data)
+    return MPO([tensor(4) for _ in range(header())])

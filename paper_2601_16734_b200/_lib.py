@@ -75,6 +75,12 @@ SIGNATURES = {
     "ttg_simplify_sum": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                     C.POINTER(C.c_void_p), C.POINTER(ttg_strategy), C.c_void_p,
                                     C.POINTER(C.c_void_p), C.POINTER(ttg_report)]),
+    "ttg_mps_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_mps_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_char_p]),
+    "ttg_mpo_load": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_mpo_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
+    "ttg_expectation_mpo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
     "ttg_scprod": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ttg_debug_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                  C.c_void_p, C.c_void_p]),

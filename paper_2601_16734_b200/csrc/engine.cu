@@ -55,6 +55,9 @@ struct ttg_ctx {
   double prof_flops[TTG_PROF_CLASSES] = {};
   int64_t prof_svd_sweeps = 0;
   int* d_sweeps = nullptr;  // device counter target for the SVD kernel (profiling)
+  // pinned double buffer of the TTLAB1 file I/O (allocated on first use)
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   void flush_profile() {
     if (pending.empty()) return;
     cudaStreamSynchronize(stream);
@@ -1026,6 +1029,10 @@ void ttg_destroy(ttg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->flush_profile();
   if (ctx->d_sweeps) cudaFree(ctx->d_sweeps);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
+    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+  }
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -1454,6 +1461,26 @@ ttg_status ttg_simplify_sum(ttg_ctx* ctx, int nterms, const double* w_re, const 
   });
 }
 
+// blas.hpp:128-138 expectation_mpo(op, u, v): <u, W v>.  The operator
+// environment chain of the reference (environments.hpp:42-63) contracts the
+// same network as the bra/ket chain over W v with the MPO bond fused into the
+// ket bond, so this is the expansion kernel (apply_raw) followed by the DMMA
+// environment chain of scprod.  Per chain; v NULL = u.
+ttg_status ttg_expectation_mpo(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* u, const ttg_dmps* v, double* out_re,
+                               double* out_im) {
+  return guarded(ctx, [&] {
+    if (!op || !u || !out_re) throw Error{TTG_INVALID, "null argument"};
+    const ttg_dmps* ket = v ? v : u;
+    if (op->n != u->n || ket->n != u->n) throw Error{TTG_SHAPE, "expectation_mpo: size mismatch"};
+    ttg_dmps* raw = nullptr;
+    ttg_status st = ttg_apply_raw(ctx, op, ket, &raw);
+    if (st != TTG_OK) throw Error{st, ttg_last_error(ctx)};
+    std::unique_ptr<ttg_dmps> guard(raw);
+    st = ttg_scprod(ctx, u, raw, out_re, out_im);
+    if (st != TTG_OK) throw Error{st, ttg_last_error(ctx)};
+  });
+}
+
 ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double* out_re, double* out_im) {
   return guarded(ctx, [&] {
     if (!u || !v || !out_re) throw Error{TTG_INVALID, "null argument"};
@@ -1517,4 +1544,296 @@ ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double
   });
 }
 
+// ---------------------------------------------------------------------------
+// TTLAB1 container on the device boundary (serialize.hpp:13-121): magic
+// "TTLAB1\0", u32 version 1, u32 tensor count, per tensor u8 rank + u64 dims
+// + complex128 row-major payload; MPS files end with the f64 error bound.
+// Payloads stream through two pinned 32 MB buffers straight into (out of)
+// the device allocations, so a file is read once and crosses PCIe once.
+// ---------------------------------------------------------------------------
+
 }  // extern "C"
+
+namespace {
+
+constexpr size_t TTLAB_STAGE = size_t(32) << 20;
+const char TTLAB_MAGIC[7] = {'T', 'T', 'L', 'A', 'B', '1', '\0'};
+
+struct File {
+  FILE* f = nullptr;
+  long long remaining = 0;  // bytes left to read (read mode)
+  File(const char* path, bool write) {
+    if (!path) throw Error{TTG_INVALID, "null path"};
+    f = std::fopen(path, write ? "wb" : "rb");
+    if (!f)
+      throw Error{TTG_NUMERIC, std::string(write ? "cannot open file for writing: " : "cannot open file for reading: ") +
+                                   path};
+    if (!write) {
+      std::fseek(f, 0, SEEK_END);
+      remaining = std::ftell(f);
+      std::fseek(f, 0, SEEK_SET);
+    }
+  }
+  ~File() {
+    if (f) std::fclose(f);
+  }
+  void read(void* p, size_t n) {
+    if ((long long)n > remaining || std::fread(p, 1, n, f) != n)
+      throw Error{TTG_NUMERIC, "ttlab container: truncated file"};
+    remaining -= (long long)n;
+  }
+  template <typename T> T pod() {
+    T v;
+    read(&v, sizeof(T));
+    return v;
+  }
+  void write(const void* p, size_t n) {
+    if (std::fwrite(p, 1, n, f) != n) throw Error{TTG_NUMERIC, "ttlab container: write failed"};
+  }
+  template <typename T> void put(T v) { write(&v, sizeof(T)); }
+  void close() {
+    if (f && std::fclose(f) != 0) {
+      f = nullptr;
+      throw Error{TTG_NUMERIC, "ttlab container: write failed"};
+    }
+    f = nullptr;
+  }
+};
+
+void stage_init(ttg_ctx* ctx) {
+  for (int i = 0; i < 2; ++i) {
+    if (!ctx->stage[i]) CK(cudaMallocHost(&ctx->stage[i], TTLAB_STAGE));
+    if (!ctx->stage_ev[i]) CK(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+  }
+}
+
+// file -> device, double-buffered: the read of chunk k+1 overlaps the copy of chunk k
+void stream_in(ttg_ctx* ctx, File& fl, void* dst, size_t bytes, int& cur) {
+  for (size_t off = 0; off < bytes; off += TTLAB_STAGE) {
+    const size_t n = std::min(TTLAB_STAGE, bytes - off);
+    CK(cudaEventSynchronize(ctx->stage_ev[cur]));
+    fl.read(ctx->stage[cur], n);
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->stage[cur], n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->stage_ev[cur], ctx->stream));
+    cur ^= 1;
+  }
+}
+
+// device -> file: the copy of chunk k+1 is in flight while chunk k is written
+void stream_out(ttg_ctx* ctx, File& fl, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  const size_t chunks = (bytes + TTLAB_STAGE - 1) / TTLAB_STAGE;
+  auto issue = [&](size_t k) {
+    const size_t off = k * TTLAB_STAGE, n = std::min(TTLAB_STAGE, bytes - off);
+    CK(cudaMemcpyAsync(ctx->stage[k & 1], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(ctx->stage_ev[k & 1], ctx->stream));
+  };
+  issue(0);
+  for (size_t k = 0; k < chunks; ++k) {
+    if (k + 1 < chunks) issue(k + 1);
+    CK(cudaEventSynchronize(ctx->stage_ev[k & 1]));
+    fl.write(ctx->stage[k & 1], std::min(TTLAB_STAGE, bytes - k * TTLAB_STAGE));
+  }
+}
+
+uint32_t read_header(File& fl) {
+  char magic[7];
+  fl.read(magic, sizeof(magic));
+  if (std::memcmp(magic, TTLAB_MAGIC, sizeof(magic)) != 0) throw Error{TTG_NUMERIC, "ttlab container: bad magic"};
+  if (fl.pod<uint32_t>() != 1u) throw Error{TTG_NUMERIC, "ttlab container: unsupported version"};
+  return fl.pod<uint32_t>();
+}
+
+void write_header(File& fl, uint32_t count) {
+  fl.write(TTLAB_MAGIC, sizeof(TTLAB_MAGIC));
+  fl.put<uint32_t>(1u);
+  fl.put<uint32_t>(count);
+}
+
+// dims of one tensor record, validated against the bytes left in the file
+std::vector<long long> read_dims(File& fl, int rank) {
+  if (fl.pod<uint8_t>() != rank)
+    throw Error{TTG_NUMERIC, rank == 3 ? "ttlab container: expected rank-3 tensor"
+                                       : "ttlab container: expected rank-4 tensor"};
+  std::vector<long long> d(rank);
+  long long elems = 1;
+  for (int i = 0; i < rank; ++i) {
+    const uint64_t x = fl.pod<uint64_t>();
+    if (x < 1) throw Error{TTG_SHAPE, rank == 3 ? "Tensor3 dimensions must be >= 1" : "Tensor4 dimensions must be >= 1"};
+    if (x > (uint64_t)fl.remaining || (elems *= (long long)x) > fl.remaining / 16)
+      throw Error{TTG_NUMERIC, "ttlab container: truncated file"};
+    d[i] = (long long)x;
+  }
+  return d;
+}
+
+// complex128 sites -> float64 when every imaginary part is zero (types.hpp:12-16: the
+// reference promotes real data to complex; the real device path gives the same
+// gauge-invariant results at a quarter of the arithmetic)
+bool all_real(ttg_ctx* ctx, const std::vector<void*>& sites, const std::vector<long long>& elems) {
+  DevBuf flag(sizeof(int), ctx->stream);
+  CK(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+  for (size_t k = 0; k < sites.size(); ++k) {
+    CK(any_imag(static_cast<const cplx*>(sites[k]), elems[k], flag.as<int>(), ctx->stream));
+    ++ctx->launches;
+  }
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return h == 0;
+}
+
+void* demote_site(ttg_ctx* ctx, void* site, long long elems) {
+  void* r = dev_alloc((size_t)elems * sizeof(double), ctx->stream);
+  CK(complex_to_real(static_cast<const cplx*>(site), static_cast<double*>(r), elems, ctx->stream));
+  ++ctx->launches;
+  cudaFreeAsync(site, ctx->stream);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+ttg_status ttg_mps_load(ttg_ctx* ctx, const char* path, int real_if_possible, ttg_dmps** out) {
+  return guarded(ctx, [&] {
+    if (!out) throw Error{TTG_INVALID, "null argument"};
+    File fl(path, false);
+    const uint32_t count = read_header(fl);
+    stage_init(ctx);
+    std::vector<int> bonds{1}, phys;
+    std::vector<long long> cap;
+    auto* m = new ttg_dmps();
+    std::unique_ptr<ttg_dmps> guard(m);
+    m->dtype = TTG_C128;
+    m->count = 1;
+    m->stream = ctx->stream;
+    int cur = 0;
+    for (uint32_t k = 0; k < count; ++k) {
+      const auto d = read_dims(fl, 3);
+      if (k == 0) bonds[0] = (int)d[0];
+      if (k > 0 && d[0] != bonds.back()) throw Error{TTG_SHAPE, "MPS bond mismatch between neighboring tensors"};
+      if (d[0] > INT32_MAX || d[1] > INT32_MAX || d[2] > INT32_MAX) throw Error{TTG_CAPACITY, "tensor dimension too large"};
+      bonds.push_back((int)d[2]);
+      phys.push_back((int)d[1]);
+      cap.push_back(d[0] * d[1] * d[2]);
+      m->site.push_back(dev_alloc((size_t)cap.back() * sizeof(cplx), ctx->stream));
+      stream_in(ctx, fl, m->site.back(), (size_t)cap.back() * sizeof(cplx), cur);
+    }
+    const double error = fl.pod<double>();
+    if (count > 0 && (bonds.front() != 1 || bonds.back() != 1))  // mps.hpp:129-133
+      throw Error{TTG_SHAPE, "MPS boundary bonds must have size one"};
+    if (error < 0) throw Error{TTG_SHAPE, "MPS error bound must be non-negative"};
+    m->n = (int)count;
+    m->phys = phys;
+    m->cap = cap;
+    m->bonds = bonds;
+    m->error.assign(1, error);
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (real_if_possible && count > 0 && all_real(ctx, m->site, cap)) {
+      for (uint32_t k = 0; k < count; ++k) m->site[k] = demote_site(ctx, m->site[k], cap[k]);
+      m->dtype = TTG_F64;
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    *out = guard.release();
+  });
+}
+
+ttg_status ttg_mps_save(ttg_ctx* ctx, const ttg_dmps* m, int chain, const char* path) {
+  return guarded(ctx, [&] {
+    if (!m) throw Error{TTG_INVALID, "null argument"};
+    if (chain < 0 || chain >= m->count) throw Error{TTG_INVALID, "chain index out of range"};
+    File fl(path, true);
+    stage_init(ctx);
+    write_header(fl, (uint32_t)m->n);
+    long long maxe = 0;
+    for (int k = 0; k < m->n; ++k) maxe = std::max(maxe, (long long)m->bond(chain, k) * m->phys[k] * m->bond(chain, k + 1));
+    std::unique_ptr<DevBuf> promo;
+    if (m->dtype == TTG_F64) promo.reset(new DevBuf((size_t)std::max(1LL, maxe) * sizeof(cplx), ctx->stream));
+    for (int k = 0; k < m->n; ++k) {
+      const long long a = m->bond(chain, k), d = m->phys[k], b = m->bond(chain, k + 1), e = a * d * b;
+      fl.put<uint8_t>(3);
+      fl.put<uint64_t>((uint64_t)a);
+      fl.put<uint64_t>((uint64_t)d);
+      fl.put<uint64_t>((uint64_t)b);
+      const char* src = static_cast<const char*>(m->site[k]) + (size_t)chain * m->cap[k] * esize(m->dtype);
+      if (m->dtype == TTG_F64) {
+        CK(real_to_complex(reinterpret_cast<const double*>(src), promo->as<cplx>(), e, ctx->stream));
+        ++ctx->launches;
+        src = static_cast<const char*>(promo->p);
+      }
+      stream_out(ctx, fl, src, (size_t)e * sizeof(cplx));
+    }
+    fl.put<double>(m->error[chain]);
+    fl.close();
+  });
+}
+
+ttg_status ttg_mpo_load(ttg_ctx* ctx, const char* path, int real_if_possible, ttg_dmpo** out) {
+  return guarded(ctx, [&] {
+    if (!out) throw Error{TTG_INVALID, "null argument"};
+    File fl(path, false);
+    const uint32_t count = read_header(fl);
+    stage_init(ctx);
+    auto* w = new ttg_dmpo();
+    std::unique_ptr<ttg_dmpo> guard(w);
+    w->dtype = TTG_C128;
+    w->stream = ctx->stream;
+    w->bonds.push_back(1);
+    std::vector<long long> elems;
+    int cur = 0;
+    for (uint32_t k = 0; k < count; ++k) {
+      const auto d = read_dims(fl, 4);
+      if (k == 0) w->bonds[0] = (int)d[0];
+      if (k > 0 && d[0] != w->bonds.back()) throw Error{TTG_SHAPE, "MPO bond mismatch between neighboring tensors"};
+      for (long long x : d)
+        if (x > INT32_MAX) throw Error{TTG_CAPACITY, "tensor dimension too large"};
+      w->dout.push_back((int)d[1]);
+      w->din.push_back((int)d[2]);
+      w->bonds.push_back((int)d[3]);
+      elems.push_back(d[0] * d[1] * d[2] * d[3]);
+      w->site.push_back(dev_alloc((size_t)elems.back() * sizeof(cplx), ctx->stream));
+      stream_in(ctx, fl, w->site.back(), (size_t)elems.back() * sizeof(cplx), cur);
+    }
+    if (count > 0 && (w->bonds.front() != 1 || w->bonds.back() != 1))
+      throw Error{TTG_SHAPE, "MPO boundary bonds must have size one"};
+    w->n = (int)count;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (real_if_possible && count > 0 && all_real(ctx, w->site, elems)) {
+      for (uint32_t k = 0; k < count; ++k) w->site[k] = demote_site(ctx, w->site[k], elems[k]);
+      w->dtype = TTG_F64;
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+    *out = guard.release();
+  });
+}
+
+ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* w, const char* path) {
+  return guarded(ctx, [&] {
+    if (!w) throw Error{TTG_INVALID, "null argument"};
+    File fl(path, true);
+    stage_init(ctx);
+    write_header(fl, (uint32_t)w->n);
+    for (int k = 0; k < w->n; ++k) {
+      const long long e = (long long)w->bonds[k] * w->dout[k] * w->din[k] * w->bonds[k + 1];
+      fl.put<uint8_t>(4);
+      fl.put<uint64_t>((uint64_t)w->bonds[k]);
+      fl.put<uint64_t>((uint64_t)w->dout[k]);
+      fl.put<uint64_t>((uint64_t)w->din[k]);
+      fl.put<uint64_t>((uint64_t)w->bonds[k + 1]);
+      std::unique_ptr<DevBuf> promo;
+      const void* src = w->site[k];
+      if (w->dtype == TTG_F64) {
+        promo.reset(new DevBuf((size_t)e * sizeof(cplx), ctx->stream));
+        CK(real_to_complex(static_cast<const double*>(src), promo->as<cplx>(), e, ctx->stream));
+        ++ctx->launches;
+        src = promo->p;
+      }
+      stream_out(ctx, fl, src, (size_t)e * sizeof(cplx));
+    }
+    fl.close();
+  });
+}
+
+}  // extern "C"
+

@@ -133,6 +133,18 @@ __global__ void fill_one_kernel(T* dst, long long s_dst, int chains) {
   if (c < chains) dst[s_dst * c] = Scalar<T>::one();
 }
 
+__global__ void any_imag_kernel(const cplx* x, long long n, int* flag) {
+  int hit = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    hit |= x[i].y != 0.0;
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void complex_to_real_kernel(const cplx* src, double* dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i].x;
+}
+
 __global__ void real_to_complex_kernel(const double* src, cplx* dst, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = cplx{src[i], 0.0};
@@ -273,6 +285,16 @@ cudaError_t copy_dims(const T* src, long long s_src, T* dst, long long s_dst, Di
 template <typename T>
 cudaError_t fill_one(T* dst, long long s_dst, int chains, cudaStream_t s) {
   fill_one_kernel<T><<<(chains + 255) / 256, 256, 0, s>>>(dst, s_dst, chains);
+  return cudaGetLastError();
+}
+
+cudaError_t any_imag(const cplx* x, long long n, int* flag, cudaStream_t s) {
+  any_imag_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t complex_to_real(const cplx* src, double* dst, long long n, cudaStream_t s) {
+  complex_to_real_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n);
   return cudaGetLastError();
 }
 

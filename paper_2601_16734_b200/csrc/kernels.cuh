@@ -41,6 +41,9 @@ template <typename T>
 cudaError_t fill_one(T* dst, long long s_dst, int chains, cudaStream_t s);
 
 cudaError_t real_to_complex(const double* src, cplx* dst, long long n, cudaStream_t s);
+// *flag |= 1 when any element of x has a non-zero imaginary part
+cudaError_t any_imag(const cplx* x, long long n, int* flag, cudaStream_t s);
+cudaError_t complex_to_real(const cplx* src, double* dst, long long n, cudaStream_t s);
 
 // MPSSum::join block (mps.hpp:352-405): dst[offl + a, s, offr + b] += f * src[a, s, b]
 // for a src tensor (a_dim x d x b_dim) inside dst (. x d x dst_right).

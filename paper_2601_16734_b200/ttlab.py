@@ -310,6 +310,13 @@ class DeviceMPO:
         self.handle, self.ctx = h, ctx
         ctx._track(h, lib.ttg_mpo_free)
 
+    @classmethod
+    def _wrap(cls, handle: C.c_void_p, ctx: Context) -> "DeviceMPO":
+        obj = cls.__new__(cls)
+        obj.handle, obj.ctx = handle, ctx
+        ctx._track(handle, lib.ttg_mpo_free)
+        return obj
+
     def __del__(self):
         try:
             if self.handle:
@@ -515,6 +522,69 @@ def scprod(u, v) -> np.ndarray:
     u.ctx.check(lib.ttg_scprod(u.ctx.handle, u.handle, v.handle, re, im))
     out = np.array(re[:]) + 1j * np.array(im[:])
     return out
+
+
+def load_mps(path, real_if_possible: bool = True, ctx: Optional[Context] = None) -> DeviceMPS:
+    """serialize.hpp:82-99 / 116-121: a TTLAB1 MPS file straight into device memory."""
+    ctx = ctx or context()
+    h = C.c_void_p()
+    ctx.check(lib.ttg_mps_load(ctx.handle, str(path).encode(), int(bool(real_if_possible)), C.byref(h)))
+    return DeviceMPS(h, ctx)
+
+
+def save_mps(path, state, chain: int = 0) -> None:
+    """serialize.hpp:67-80 / 108-113 (one chain of a batch)."""
+    state = _as_mps(state)
+    state.ctx.check(lib.ttg_mps_save(state.ctx.handle, state.handle, int(chain), str(path).encode()))
+
+
+def load_mpo(path, real_if_possible: bool = True, ctx: Optional[Context] = None) -> DeviceMPO:
+    """serialize.hpp:101-121 (MPO)."""
+    ctx = ctx or context()
+    h = C.c_void_p()
+    ctx.check(lib.ttg_mpo_load(ctx.handle, str(path).encode(), int(bool(real_if_possible)), C.byref(h)))
+    return DeviceMPO._wrap(h, ctx)
+
+
+def save_mpo(path, op) -> None:
+    op = _as_mpo(op)
+    op.ctx.check(lib.ttg_mpo_save(op.ctx.handle, op.handle, str(path).encode()))
+
+
+def expectation_mpo(op, u, v=None) -> np.ndarray:
+    """blas.hpp:128-138: <u, op v> per chain (v defaults to u)."""
+    u = _as_mps(u)
+    dv = None if v is None else _as_mps(v, u.ctx)
+    dop = _as_mpo(op, u.ctx)
+    cnt = u.count
+    re, im = (C.c_double * cnt)(), (C.c_double * cnt)()
+    u.ctx.check(lib.ttg_expectation_mpo(u.ctx.handle, dop.handle, u.handle, None if dv is None else dv.handle, re, im))
+    return np.array(re[:]) + 1j * np.array(im[:])
+
+
+def expectation_local(v, op, site: int, op2=None, site2: Optional[int] = None) -> np.ndarray:
+    """blas.hpp:100-125: <v, O_site v> or the two-point <v, O_site O2_site2 v>
+    (not normalised).  The local operators become a bond-1 MPO (identity on
+    the other sites) evaluated by `expectation_mpo` on the device."""
+    v = _as_mps(v)
+    info = v.info()
+    L, phys = info["n"], info["phys"]
+    if site < 0 or site >= L:
+        raise ShapeError("expectation_local: site out of range")
+    if (op2 is None) != (site2 is None):
+        raise ShapeError("expectation_local: two-point value needs both operator and site")
+    if op2 is not None and (site2 < 0 or site2 >= L or site2 == site):
+        raise ShapeError("expectation_local: second site out of range")
+    ops = {site: op}
+    if op2 is not None:
+        ops[site2] = op2
+    tensors = []
+    for n in range(L):
+        m = np.asarray(ops.get(n, np.eye(phys[n])))
+        if m.shape != (phys[n], phys[n]):
+            raise ShapeError("local operator dimension mismatch")
+        tensors.append(m.reshape(1, phys[n], phys[n], 1))
+    return expectation_mpo(tensors, v)
 
 
 def norm(v) -> np.ndarray:

@@ -8,6 +8,9 @@
 
 #include "ttlab/blas.hpp"
 #include "ttlab/qft.hpp"
+#include "ttlab/serialize.hpp"
+
+#include <sstream>
 
 using namespace ttlab;
 
@@ -219,6 +222,47 @@ int main() {
     }
     CHECK(dist(mps_to_dense(qft_flip(qft(u))), expected) < 1e-10);
     CHECK(dist(mps_to_dense(qft_flip(qft_flip(u))), x) == 0.0);
+  });
+  section("expectation_mpo: identity = scprod (test_blas.cpp:170-174)", [] {
+    MPS u = random_uniform_mps(4, 2, 2, 17), v = random_uniform_mps(4, 2, 3, 18);
+    CHECK(std::abs(expectation_mpo(mpo_identity(4, 2), u, v) - scprod(u, v)) < 1e-12);
+    CHECK(std::abs(expectation_mpo(mpo_identity(4, 2), u) - u.norm_squared()) < 1e-12);
+  });
+  section("serialization round trip is bit exact; device loader reads the same file (test_core.cpp:229-256)", [] {
+    MPS state = random_uniform_mps(5, 2, 4, 123);
+    state.set_error(0.125);
+    std::stringstream buffer;
+    save_mps(buffer, state);
+    MPS loaded = load_mps(buffer);
+    CHECK(loaded.size() == state.size());
+    CHECK(loaded.error() == state.error());
+    for (index_t n = 0; n < state.size(); ++n)
+      CHECK(std::memcmp(loaded[n].data(), state[n].data(), sizeof(cplx) * static_cast<size_t>(state[n].size())) == 0);
+    MPO op = mpo_identity(3, 2);
+    std::stringstream obuf;
+    save_mpo(obuf, op);
+    MPO oload = load_mpo(obuf);
+    CHECK(oload.size() == op.size());
+    bool threw = false;
+    try {
+      std::stringstream bad("garbage");
+      load_mps(bad);
+    } catch (const numeric_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+    const std::string path = "/tmp/ttgpu_dropin_state.ttlab";
+    save_mps(path, state);
+    ttg_dmps* d = nullptr;
+    gpu::check(gpu::ctx(), ttg_mps_load(gpu::ctx(), path.c_str(), 1, &d));
+    gpu::DMps dm(d);
+    double err = 0.0;
+    auto ts = gpu::download(dm.h, 0, &err, nullptr);
+    CHECK(err == 0.125);
+    for (index_t n = 0; n < state.size(); ++n)
+      CHECK(std::memcmp(ts[static_cast<size_t>(n)].data(), state[n].data(),
+                        sizeof(cplx) * static_cast<size_t>(state[n].size())) == 0);
+    std::remove(path.c_str());
   });
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;

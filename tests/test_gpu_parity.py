@@ -311,3 +311,30 @@ def test_config3_reduced_parity():
     if rep[0]["sweeps"] != rr["sweeps"]:
         assert len(d) >= 2 and abs(d[-1] - d[-2]) <= 1e-12 * rr["target_norm2"]
     _check_config_parity(out, rep[0], ref, rr, np.sqrt(rr["target_norm2"]))
+
+
+def test_expectations():
+    """test_blas.cpp:155-178 on the device, plus a Laplacian expectation at
+    config-2 scale against the oracle's operator environments."""
+    t = T()
+    from oracle.rng import random_matrix
+    sz = np.diag([1.0, -1.0])
+    assert abs(t.expectation_local(O.basis_state(3, 2, 0).tensors, sz, 0)[0] - 1.0) < 1e-15
+    assert abs(t.expectation_local(O.basis_state(2, 2, 1).tensors, sz, 0, sz, 1)[0] + 1.0) < 1e-15
+    v = O.random_uniform_mps(4, 2, 3, 16)
+    op, op2 = random_matrix(2, 2, 40), random_matrix(2, 2, 41)
+    assert abs(t.expectation_local(v.tensors, op, 2)[0] - O.expectation_local(v, op, 2)) < 1e-12
+    assert abs(t.expectation_local(v.tensors, op, 1, op2, 3)[0] - O.expectation_local(v, op, 1, op2, 3)) < 1e-12
+    u, w = O.random_uniform_mps(4, 2, 2, 17), O.random_uniform_mps(4, 2, 3, 18)
+    assert abs(t.expectation_mpo(O.mpo_identity(4, 2).tensors, u.tensors, w.tensors)[0] - O.scprod(u, w)) < 1e-12
+    mpo = O.mpo_from_local_operators([random_matrix(2, 2, s) for s in (51, 52, 53, 54)])
+    assert abs(t.expectation_mpo(mpo.tensors, u.tensors, w.tensors)[0] - O.expectation_mpo(mpo, u, w)) < 1e-12
+    with pytest.raises(t.ShapeError):
+        t.expectation_mpo(O.mpo_identity(3, 2).tensors, u.tensors)
+    with pytest.raises(t.ShapeError):
+        t.expectation_local(v.tensors, op, 1, op2, 1)
+    psi = I.random_mps(12, 2, 16, 7)
+    W = I.laplacian_mpo(12)
+    got = t.expectation_mpo(W, psi)[0]
+    ref = O.expectation_mpo(O.MPO(W), omps(psi))
+    assert abs(got - ref) <= 1e-12 * max(abs(ref), 1.0)

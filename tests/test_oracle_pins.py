@@ -217,3 +217,55 @@ def test_two_site_linear_form_pins_projection():
             f = proj(L, w[n], w[n + 1], R)
             pair = O.join_pair(v[n], v[n + 1])
             assert abs(np.vdot(pair, f) - ref) < 1e-12
+
+
+def test_expectation_pins():
+    """test_blas.cpp:155-178 against dense contractions."""
+    sz = np.diag([1.0, -1.0])
+    assert abs(O.expectation_local(O.basis_state(3, 2, 0), sz, 0) - 1.0) < 1e-15
+    assert abs(O.expectation_local(O.basis_state(2, 2, 1), sz, 0, sz, 1) + 1.0) < 1e-15
+    v = O.random_uniform_mps(4, 2, 3, 16)
+    d = O.mps_to_dense(v)
+    op, op2 = random_matrix(2, 2, 40), random_matrix(2, 2, 41)
+    emb = lambda m, k: np.kron(np.kron(np.eye(2 ** k), m), np.eye(2 ** (3 - k)))
+    assert abs(O.expectation_local(v, op, 2) - np.vdot(d, emb(op, 2) @ d)) < 1e-12
+    assert abs(O.expectation_local(v, op, 1, op2, 3) - np.vdot(d, emb(op, 1) @ emb(op2, 3) @ d)) < 1e-12
+    u, w = O.random_uniform_mps(4, 2, 2, 17), O.random_uniform_mps(4, 2, 3, 18)
+    assert abs(O.expectation_mpo(O.mpo_identity(4, 2), u, w) - O.scprod(u, w)) < 1e-12
+    mpo = O.mpo_from_local_operators([random_matrix(2, 2, s) for s in (51, 52, 53, 54)])
+    ref = np.vdot(O.mps_to_dense(u), O.mpo_to_dense(mpo) @ O.mps_to_dense(w))
+    assert abs(O.expectation_mpo(mpo, u, w) - ref) < 1e-12
+    with pytest.raises(O.ShapeError):
+        O.expectation_local(v, op, 4)
+    with pytest.raises(O.ShapeError):
+        O.expectation_local(v, op, 1, op2, 1)
+    with pytest.raises(O.ShapeError):
+        O.expectation_local(v, np.eye(3), 1)
+
+
+def test_ttlab1_container_pins():
+    """test_core.cpp:229-256 (bit-exact round trip, bad magic) and the byte layout
+    of serialize.hpp:13-16 assembled independently with struct."""
+    import struct
+    state = O.random_uniform_mps(5, 2, 4, 123)
+    state.error = 0.125
+    blob = O.dumps_mps(state)
+    back = O.loads_mps(blob)
+    assert back.error == 0.125 and len(back) == 5
+    for a, b in zip(back.tensors, state.tensors):
+        assert a.shape == b.shape and a.tobytes() == b.astype(np.complex128).tobytes()
+    t0 = state.tensors[0]
+    head = b"TTLAB1\0" + struct.pack("<I", 1) + struct.pack("<I", 5)
+    rec0 = struct.pack("<B", 3) + struct.pack("<QQQ", *t0.shape)
+    assert blob.startswith(head + rec0)
+    assert blob[len(head) + len(rec0):len(head) + len(rec0) + 16] == struct.pack("<dd", t0[0, 0, 0].real, t0[0, 0, 0].imag)
+    assert blob.endswith(struct.pack("<d", 0.125))
+    op = O.mpo_identity(3, 2)
+    ob = O.loads_mpo(O.dumps_mpo(op))
+    assert all(np.array_equal(a, b) for a, b in zip(ob.tensors, op.tensors))
+    with pytest.raises(O.NumericError):
+        O.loads_mps(b"garbage")
+    with pytest.raises(O.NumericError):
+        O.loads_mps(blob[:-9])
+    with pytest.raises(O.NumericError):
+        O.loads_mps(O.dumps_mpo(op))  # rank-4 record in an MPS file
