@@ -192,6 +192,10 @@ ttg_status ttg_debug_svd_ex(int dtype, int m, int n, const void* theta, int mode
 ttg_status ttg_debug_qr(int dtype, int m, int n, const void* A, void* Q, void* R);
 /* Same factorisation through the blocked path (panel kernel + DMMA WY updates). */
 ttg_status ttg_debug_qr_blocked(int dtype, int m, int n, const void* A, void* Q, void* R);
+/* Split preconditioner: M = A (trans 0) or A^H (trans 1) = Q R; writes Q (l x r0, nullable) and
+ * R^H (k x r0).  small = 1: blocked shared-memory kernel (qr_small.cu); 0: the unblocked kernel. */
+ttg_status ttg_debug_qr_pre(int dtype, int m, int n, int trans, const void* A, void* Q, void* RH, int small,
+                            double* ms);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -93,6 +93,8 @@ SIGNATURES = {
                                    C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_double]),
     "ttg_debug_qr": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ttg_debug_qr_blocked": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ttg_debug_qr_pre": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                    C.POINTER(C.c_double)]),
 }
 
 

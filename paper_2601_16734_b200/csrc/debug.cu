@@ -137,9 +137,46 @@ ttg_status do_qr_blocked(int m, int n, const void* A, void* Q, void* R) {
   return TTG_OK;
 }
 
+// qr_precondition on one l x k matrix M = A (trans 0) or A^H (trans 1), A m x n row-major
+template <typename T>
+ttg_status do_qr_pre(int m, int n, int trans, const void* A, void* Q, void* RH, int small, double* ms) {
+  const size_t es = sizeof(T);
+  const int l = trans ? n : m, k = trans ? m : n, r0 = l < k ? l : k;
+  Buf a((size_t)m * n * es), q((size_t)l * r0 * es), rh((size_t)k * r0 * es), bonds(4 * sizeof(int));
+  cudaMemcpy(a.p, A, (size_t)m * n * es, cudaMemcpyHostToDevice);
+  cudaMemset(bonds.p, 0, 4 * sizeof(int));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, nullptr);
+  cudaError_t e = small ? qr_precondition_small<T>(a.p, 0, dconst(m), dconst(n), trans, static_cast<int*>(bonds.p), 4,
+                                                   0, Q ? q.p : nullptr, 0, rh.p, 0, l, k, nullptr, 1, nullptr)
+                        : qr_precondition_unblocked<T>(a.p, 0, dconst(m), dconst(n), trans,
+                                                       static_cast<int*>(bonds.p), 4, 0, Q ? q.p : nullptr, 0, rh.p, 0,
+                                                       l, k, nullptr, 1, nullptr);
+  cudaEventRecord(e1, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  float f = 0.f;
+  cudaEventElapsedTime(&f, e0, e1);
+  if (ms) *ms = f;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (e != cudaSuccess) return TTG_CUDA;
+  if (Q) cudaMemcpy(Q, q.p, (size_t)l * r0 * es, cudaMemcpyDeviceToHost);
+  cudaMemcpy(RH, rh.p, (size_t)k * r0 * es, cudaMemcpyDeviceToHost);
+  return TTG_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+ttg_status ttg_debug_qr_pre(int dtype, int m, int n, int trans, const void* A, void* Q, void* RH, int small,
+                            double* ms) {
+  if (m < 1 || n < 1) return TTG_INVALID;
+  return dtype == TTG_F64 ? do_qr_pre<double>(m, n, trans, A, Q, RH, small, ms)
+                          : do_qr_pre<cplx>(m, n, trans, A, Q, RH, small, ms);
+}
 
 ttg_status ttg_debug_qr_blocked(int dtype, int m, int n, const void* A, void* Q, void* R) {
   if (m < 1 || n < 1) return TTG_INVALID;

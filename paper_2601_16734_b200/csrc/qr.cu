@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 namespace ttg {
 namespace {
@@ -408,6 +409,20 @@ template <typename T>
 cudaError_t qr_precondition(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
                             int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
                             const ChainState* st, int chains, cudaStream_t s) {
+  static const bool small_off = [] {
+    const char* e = std::getenv("TTG_QR_SMALL");
+    return e && e[0] == '0';
+  }();
+  if (!small_off && lmax <= 256 && qr_small_bytes(lmax, kmax, Scalar<T>::is_complex) <= QR_SMALL_SMEM_LIMIT)
+    return qr_precondition_small<T>(A, sA, M, N, trans, bonds, ld, out_idx, Q, sQ, RH, sRH, lmax, kmax, st, chains, s);
+  return qr_precondition_unblocked<T>(A, sA, M, N, trans, bonds, ld, out_idx, Q, sQ, RH, sRH, lmax, kmax, st, chains,
+                                      s);
+}
+
+template <typename T>
+cudaError_t qr_precondition_unblocked(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
+                                      int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
+                                      const ChainState* st, int chains, cudaStream_t s) {
   const size_t bytes = (size_t)(lmax | 1) * kmax * sizeof(T);
   if (bytes > QR_R_SMEM_LIMIT || (lmax < kmax ? lmax : kmax) > 1024) return cudaErrorInvalidValue;
   cudaError_t e =
@@ -418,6 +433,12 @@ cudaError_t qr_precondition(const void* A, long long sA, DimExpr M, DimExpr N, i
   return cudaGetLastError();
 }
 
+template cudaError_t qr_precondition_unblocked<double>(const void*, long long, DimExpr, DimExpr, int, int*, int, int,
+                                                       void*, long long, void*, long long, int, int,
+                                                       const ChainState*, int, cudaStream_t);
+template cudaError_t qr_precondition_unblocked<cplx>(const void*, long long, DimExpr, DimExpr, int, int*, int, int,
+                                                     void*, long long, void*, long long, int, int, const ChainState*,
+                                                     int, cudaStream_t);
 template cudaError_t qr_precondition<double>(const void*, long long, DimExpr, DimExpr, int, int*, int, int, void*,
                                              long long, void*, long long, int, int, const ChainState*, int,
                                              cudaStream_t);

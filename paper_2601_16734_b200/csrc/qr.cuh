@@ -37,6 +37,20 @@ cudaError_t qr_precondition(const void* A, long long sA, DimExpr M, DimExpr N, i
                             int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
                             const ChainState* st, int chains, cudaStream_t s);
 
+// Blocked variant of qr_precondition for l <= 256 and a panel that fits one
+// CTA's shared memory (qr_small.cu): warp-level register panels + block
+// reflector updates.  Returns cudaErrorInvalidValue when not applicable.
+constexpr size_t QR_SMALL_SMEM_LIMIT = 216 * 1024;
+size_t qr_small_bytes(int l, int k, bool cplx_);
+template <typename T>
+cudaError_t qr_precondition_unblocked(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
+                                      int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
+                                      const ChainState* st, int chains, cudaStream_t s);
+template <typename T>
+cudaError_t qr_precondition_small(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld,
+                                  int out_idx, void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax,
+                                  const ChainState* st, int chains, cudaStream_t s);
+
 template <typename T>
 cudaError_t qr_r_factor(const void* A, long long sA, DimExpr M, DimExpr N, int* bonds, int ld, int out_idx, void* R,
                         long long sR, int mmax, int nmax, int chains, cudaStream_t s);

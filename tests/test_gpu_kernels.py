@@ -165,3 +165,53 @@ def test_svd_rank_deficient_drops_zero_values(svd_impl):
     _, sv, r, _ = _svd(th, 0, tol=1e-12)
     assert r == 5
     assert sv[5] < 1e-12 * sv[0]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+@pytest.mark.parametrize("shape,trans", [((128, 128), 0), ((128, 128), 1), ((64, 64), 0), ((100, 37), 0),
+                                         ((37, 100), 1), ((200, 96), 0), ((24, 80), 0), ((250, 60), 0),
+                                         ((17, 5), 1), ((128, 40), 1)])
+def test_qr_precondition_small_kernel(dtype, shape, trans):
+    """qr_small.cu (blocked, register panels) against the definition M = Q R and
+    against the unblocked preconditioner it replaces."""
+    lib = _lib()
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    A = rng.standard_normal((m, n))
+    if dtype == np.complex128:
+        A = A + 1j * rng.standard_normal((m, n))
+    A = np.ascontiguousarray(A)
+    M = A.conj().T if trans else A
+    l, k = M.shape
+    r0 = min(l, k)
+    code = 1 if dtype == np.complex128 else 0
+    if 16 * l * k > 200 * 1024 and code == 1:
+        pytest.skip("complex panel does not fit shared memory")
+    out = {}
+    for small in (1, 0):
+        Q = np.empty((l, r0), dtype=dtype)
+        RH = np.empty((k, r0), dtype=dtype)
+        ms = C.c_double()
+        assert lib.ttg_debug_qr_pre(code, m, n, trans, _ptr(A), _ptr(Q), _ptr(RH), small, C.byref(ms)) == 0
+        R = RH.conj().T
+        assert np.abs(Q.conj().T @ Q - np.eye(r0)).max() < 1e-13
+        assert np.abs(Q @ R - M).max() < 1e-12 * np.abs(M).max()
+        assert np.abs(np.tril(R, -1)).max() == 0.0
+        out[small] = (Q, R)
+        # R only (no Q)
+        RH2 = np.empty((k, r0), dtype=dtype)
+        assert lib.ttg_debug_qr_pre(code, m, n, trans, _ptr(A), None, _ptr(RH2), small, C.byref(ms)) == 0
+        assert np.array_equal(RH2, RH)
+    # same Householder convention: identical factors up to rounding
+    assert np.abs(out[1][1] - out[0][1]).max() < 1e-12 * np.abs(M).max()
+
+
+def test_qr_precondition_small_rank_deficient():
+    lib = _lib()
+    rng = np.random.default_rng(11)
+    A = np.ascontiguousarray(rng.standard_normal((128, 5)) @ rng.standard_normal((5, 128)))
+    Q = np.empty((128, 128))
+    RH = np.empty((128, 128))
+    assert lib.ttg_debug_qr_pre(0, 128, 128, 0, _ptr(A), _ptr(Q), _ptr(RH), 1, None) == 0
+    assert np.abs(Q.T @ Q - np.eye(128)).max() < 1e-13
+    assert np.abs(Q @ RH.T - A).max() < 1e-12 * np.abs(A).max()
