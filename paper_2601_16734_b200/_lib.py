@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libttgpu.so")
+LIB_PATH = os.environ.get("TTG_LIB", os.path.join(_HERE, "libttgpu.so"))  # TTG_LIB: A/B builds (tools)
 
 TTG_OK, TTG_SHAPE, TTG_CAPACITY, TTG_NUMERIC, TTG_CUDA, TTG_INVALID = range(6)
 TTG_F64, TTG_C128 = 0, 1

@@ -319,7 +319,14 @@ struct Engine {
                   s_work);
       return;
     }
-    if (!no_pre && pre_ok && pre_buf && !grid_path && w.pre == nullptr && (long long)mu * nu >= 24 * 24 &&
+    // splits within 32 x 32: the two preconditioning QRs cost more than the
+    // Jacobi sweeps they save (tools/split_probe.py, C1)
+    static const int pre_skip = [] {
+      const char* e = getenv("TTG_PRE_SKIP");
+      return e ? atoi(e) : 32;
+    }();
+    if (!no_pre && pre_ok && pre_buf && !grid_path && w.pre == nullptr && std::min(mu, nu) >= 24 &&
+        std::max(mu, nu) > pre_skip &&
         (size_t)(std::max(mu, nu) | 1) * std::max(mu, nu) * sizeof(T) <= QR_R_SMEM_LIMIT && std::min(mu, nu) <= 1024 &&
         (long long)std::max(mu, nu) * std::max(mu, nu) <= pre_cap) {
       split_preconditioned(theta, s_theta, M, N, out_idx, iso, s_iso, mode, tol, max_bond, check_active, accumulate,
