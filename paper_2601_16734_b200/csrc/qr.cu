@@ -1024,6 +1024,200 @@ __global__ void __launch_bounds__(COOP_THREADS) qr_panel_coop_kernel(T* A, int l
 }
 
 template <typename T>
+__device__ __forceinline__ T shfl_t(T v, int src) {
+  if constexpr (Scalar<T>::is_complex)
+    return cplx{__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
+  else
+    return __shfl_sync(0xffffffffu, v, src);
+}
+__device__ __forceinline__ double fma_c(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ cplx fma_c(cplx a, cplx b, cplx c) {
+  return cplx{fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y))};
+}
+__device__ __forceinline__ double re_of(double a) { return a; }
+__device__ __forceinline__ double re_of(cplx a) { return a.x; }
+
+// Single-chain panels, one thread-block cluster (C <= 16 CTAs): lanes own the
+// panel's columns (lane c = column c) and every warp a contiguous slab of RW
+// rows, all in registers, so column j is simply lane j (shuffles, no dynamic
+// register indexing).  Per column ONE 32-value reduction: lane c accumulates
+// q_c = sum_{rows > j} conj(P_c) x over its rows (x = column j): q_j = |x|^2,
+// q_c (c > j) = conj(x^H a_c), q_c (c < j) = V_c^H x (the Gram column of the
+// WY factor).  Warp partials -> CTA partial (shared) -> pushed into every
+// CTA of the cluster (DSMEM), one cluster barrier, then every warp forms the
+// same reflector (xLARFG convention) and updates its rows.  Partial slots are
+// double-buffered by column parity, so one barrier per column suffices.
+template <typename T, int RW, int NT>
+__global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int mp, int jb, T* Vall, int ldv, T* Tp) {
+  constexpr bool CPX = Scalar<T>::is_complex;
+  constexpr int NW = NT / 32;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), b = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ T wpart[NW][32];
+  __shared__ T slot[2][16][32];
+  __shared__ T rowj[2][32];
+  __shared__ T taus[QR_NB];
+  __shared__ T S[QR_NB][QR_NB + 1];
+  const int g0 = (b * NW + warp) * RW;  // first row of this warp's slab
+  const bool colv = lane < jb;
+  T a[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int g = g0 + r;
+    a[r] = (colv && g < mp) ? A[(size_t)g * lda + lane] : Scalar<T>::zero();
+  }
+  const int jr = jb < mp ? jb : mp;
+  for (int j = 0; j < jr; ++j) {
+    const int par = j & 1;
+    // ---- partials
+    T q = Scalar<T>::zero(), q2 = Scalar<T>::zero();
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const T x = shfl_t(a[r], j);
+      const T y = (g0 + r > j) ? x : Scalar<T>::zero();
+      if (r & 1)
+        q2 = fma_c(conj_(a[r]), y, q2);
+      else
+        q = fma_c(conj_(a[r]), y, q);
+    }
+    q = add(q, q2);
+    // the owner of row j publishes it to every CTA
+    if (j >= g0 && j < g0 + RW) {
+      T rv = Scalar<T>::zero();
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+        if (g0 + r == j) rv = a[r];
+      for (int g = 0; g < C; ++g) cl.map_shared_rank(&rowj[par][0], g)[lane] = rv;
+    }
+    wpart[warp][lane] = q;
+    __syncthreads();
+    if (warp == 0) {
+      T s = wpart[0][lane];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) s = add(s, wpart[w][lane]);
+      for (int g = 0; g < C; ++g) cl.map_shared_rank(&slot[par][0][0], g)[b * 32 + lane] = s;
+    }
+    cl.sync();
+    // ---- reflector (every warp, redundantly)
+    T t = slot[par][0][lane];
+    for (int g = 1; g < C; ++g) t = add(t, slot[par][g][lane]);
+    const double xn2 = re_of(shfl_t(t, j));
+    const T alpha = rowj[par][j];
+    double ar, ai;
+    if constexpr (CPX) {
+      ar = alpha.x;
+      ai = alpha.y;
+    } else {
+      ar = alpha;
+      ai = 0.0;
+    }
+    T tau = Scalar<T>::zero(), sc = Scalar<T>::one();
+    double beta = ar;
+    const bool refl = !(xn2 == 0.0 && ai == 0.0);
+    if (refl) {
+      beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+      const double rb = 1.0 / beta;
+      if constexpr (CPX) {
+        tau = cplx{(beta - ar) * rb, -ai * rb};
+        const double dr = ar - beta, di = ai, rden = 1.0 / (dr * dr + di * di);
+        sc = cplx{dr * rden, -di * rden};
+      } else {
+        tau = (beta - ar) * rb;
+        sc = 1.0 / (ar - beta);
+      }
+    }
+    const T pj = rowj[par][lane];  // P(j, c)
+    // f_c = conj(tau) (a_c(j) + conj(sc) d_c), d_c = conj(t_c)  (c > j)
+    const T f = mul(conj_(tau), add(pj, mul(conj_(sc), conj_(t))));
+    if (warp == 0 && lane < j) S[lane][j] = add(conj_(pj), mul(sc, t));  // V_c^H v_j
+    if (tid == 0) taus[j] = tau;
+    // ---- update: lane j stores v (rows > j) and beta; lanes c > j: a_c -= v f_c
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int g = g0 + r;
+      const T x = shfl_t(a[r], j);
+      const T v = (g > j) ? mul(x, sc) : (g == j ? Scalar<T>::one() : Scalar<T>::zero());
+      T nv = a[r];
+      if (lane > j) nv = sub(a[r], mul(v, f));
+      if (lane == j) {
+        if (g > j) nv = v;
+        else if (g == j && refl) {
+          if constexpr (CPX)
+            nv = cplx{beta, 0.0};
+          else
+            nv = beta;
+        }
+      }
+      a[r] = nv;
+    }
+  }
+  // ---- write back R (upper part) and V (unit lower trapezoid)
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int g = g0 + r;
+    if (colv && g < mp) {
+      A[(size_t)g * lda + lane] = a[r];
+      Vall[(size_t)g * ldv + lane] =
+          (lane >= jr) ? Scalar<T>::zero() : (g > lane ? a[r] : (g == lane ? Scalar<T>::one() : Scalar<T>::zero()));
+    }
+  }
+  if (b == 0) {
+    __syncthreads();
+    if (warp == 0) warp_larft<T>(S, taus, jr, lane, Tp);
+  }
+  cl.sync();  // no CTA leaves while peers may still write into its shared memory
+}
+
+template <typename T, int RW>
+cudaError_t launch_panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* Tp, cudaStream_t s) {
+  constexpr int NT = 512;
+  const int rows_cta = (NT / 32) * RW;
+  const int C = (mp + rows_cta - 1) / rows_cta;
+  if (C > 16) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qr_panel_cl_kernel<T, RW, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qr_panel_cl_kernel<T, RW, NT>, Ap, lda, mp, jb, Vp, ldv, Tp);
+}
+
+// Rows per warp for an mp-row panel: the smallest slab that keeps the cluster
+// at <= 8 CTAs (<= 16 for the tallest panels); 0 = not eligible.
+template <typename T>
+cudaError_t panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* Tp, cudaStream_t s) {
+  constexpr int RWMAX = Scalar<T>::is_complex ? 16 : 32;
+  if (mp <= 8 * 16 * 4) return launch_panel_cl<T, 4>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  if (mp <= 8 * 16 * 8) return launch_panel_cl<T, 8>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  if (mp <= 16 * 16 * 16 || RWMAX == 16) return launch_panel_cl<T, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  return launch_panel_cl<T, RWMAX>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+}
+
+bool panel_cl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TTG_QR_CL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename T> int panel_cl_max_rows() { return Scalar<T>::is_complex ? 16 * 16 * 16 : 16 * 16 * 32; }
+
+template <typename T>
 __global__ void conj_transpose_kernel(const T* src, long long s_src, int rows, int cols, T* dst, long long s_dst) {
   __shared__ T tile[32][33];
   const int chain = blockIdx.z;
@@ -1141,7 +1335,11 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     const int mp = m - j0;
     const size_t pbytes = (size_t)mp * jb * sizeof(T);
     const int in_smem = pbytes <= smem_limit;
-    if (in_smem) {
+    if (chains == 1 && panel_cl_enabled() && mp <= panel_cl_max_rows<T>()) {
+      e = panel_cl<T>(A + (size_t)j0 * n + j0, n, mp, jb, V + (size_t)j0 * k + j0, k,
+                      Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, s);
+      if (e != cudaSuccess) return e;
+    } else if (in_smem) {
       qr_panel_kernel<T><<<chains, PANEL_THREADS, pbytes, s>>>(
           A + (size_t)j0 * n + j0, w.sA, n, mp, jb, V + (size_t)j0 * k + j0, w.sV, k,
           Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP, 1);
