@@ -246,6 +246,28 @@ def _workload_desc(cfg):
     return f"{cfg.name}: n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS (seed {cfg.seed}+1000*rank), " + tail
 
 
+def _roofline(prof):
+    """Roofline of the dominant kernel class of a profiled call (CUDA events around
+    every launch, executed flops from the live bond table)."""
+    dom = max(("gemm", "svd", "qr"), key=lambda k: prof[k]["ms"])
+    p = prof[dom]
+    achieved = p["flops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
+    return {
+        "bound": "fp64",
+        "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)", "svd": "ttg::jacobi_svd_kernel",
+                   "qr": "ttg::qr_kernel"}[dom],
+        "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+        "per_launch": {"launches_per_step": p["launches"], "avg_us": 1e3 * p["ms"] / max(1, p["launches"]),
+                       "flops_per_launch": p["flops"] / max(1, p["launches"])},
+        "share_of_step": {k: v["ms"] / max(1e-9, sum(x["ms"] for x in prof.values())) for k, v in prof.items()},
+        "peak_source": "measured FP64 DMMA (mma.sync m16n8k4) 37.07 TF/s on this pool, tools/fp64_peak; "
+                       "MEASURED_PEAKS.json has no FP64 entry; DFMA measured 36.8 TF/s, cuBLAS DGEMM 35.5",
+        "flops_model": "executed flops: 2MNK per GEMM from the live bond table; SVD = Golub-Van Loan "
+                       "4m^2n+8mn^2+9n^3; QR = 4n^2(m-n/3)",
+    }
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -350,23 +372,7 @@ def run_ours(args):
         _call(ttlab, cfg, mpsd, Wd, strat)
         prof = ctx.profile_read()
         ctx.profile_enable(False)
-        dom = max(("gemm", "svd", "qr"), key=lambda k: prof[k]["ms"])
-        p = prof[dom]
-        achieved = p["flops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
-        roofline = {
-            "bound": "fp64",
-            "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)", "svd": "ttg::jacobi_svd_kernel",
-                       "qr": "ttg::qr_kernel"}[dom],
-            "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
-            "per_launch": {"launches_per_step": p["launches"], "avg_us": 1e3 * p["ms"] / max(1, p["launches"]),
-                           "flops_per_launch": p["flops"] / max(1, p["launches"])},
-            "share_of_step": {k: v["ms"] / max(1e-9, sum(x["ms"] for x in prof.values())) for k, v in prof.items()},
-            "peak_source": "measured FP64 DMMA (mma.sync m16n8k4) 37.07 TF/s on this pool, tools/fp64_peak; "
-                           "MEASURED_PEAKS.json has no FP64 entry; DFMA measured 36.8 TF/s, cuBLAS DGEMM 35.5",
-            "flops_model": "executed flops: 2MNK per GEMM from the live bond table; SVD = Golub-Van Loan "
-                           "4m^2n+8mn^2+9n^3; QR = 4n^2(m-n/3)",
-        }
+        roofline = _roofline(prof)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -521,6 +527,7 @@ def run_ours_batch(args):
         step(batch)
         prof = ctx.profile_read()
         ctx.profile_enable(False)
+    roofline = _roofline(prof) if prof else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -543,7 +550,7 @@ def run_ours_batch(args):
             "chains_per_s": total * args.steps / (ms_max / 1e3),
             "e2e": {"value": e2e_value, "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": int(launches), "profile": prof, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": int(launches), "roofline": roofline, "profile": prof, "cpu_baseline": cpu, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

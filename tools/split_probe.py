@@ -10,6 +10,7 @@ sys.path.insert(0, ".")
 from paper_2601_16734_b200._lib import lib  # noqa: E402
 
 REPS = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+QR_KIND = int(__import__("os").environ.get("QR_KIND", "1"))  # 1 qr_small, 0 unblocked
 
 
 def svd(th, mode=0):
@@ -39,7 +40,7 @@ def qr_pre(A, withq):
     best = 1e9
     for _ in range(REPS):
         st = lib.ttg_debug_qr_pre(0, m, n, 0, C.c_void_p(A.ctypes.data), C.c_void_p(Q.ctypes.data) if withq else None,
-                                  C.c_void_p(RH.ctypes.data), 1, C.byref(ms))
+                                  C.c_void_p(RH.ctypes.data), QR_KIND, C.byref(ms))
         assert st == 0, st
         best = min(best, ms.value * 1e3)
     return best
