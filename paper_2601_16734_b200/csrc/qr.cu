@@ -1275,12 +1275,51 @@ template <typename T>
 size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t* sW, size_t* sP) {
   const int k = m < n ? m : n;
   const int nblk = (k + QR_NB - 1) / QR_NB;
+  const int nblko = (k + QR_NBO - 1) / QR_NBO;
   *sA = (size_t)m * n;
   *sV = (size_t)m * k;
-  *sT = (size_t)nblk * QR_NB * QR_NB;
-  *sW = (size_t)QR_NB * n;
+  // inner 32 x 32 WY factors | outer 128 x 128 WY factors | S = V_O^H V_O scratch
+  *sT = (size_t)nblk * QR_NB * QR_NB + (size_t)(nblko + 1) * QR_NBO * QR_NBO;
+  *sW = (size_t)QR_NBO * n;
   *sP = (size_t)m * QR_NB;
   return *sA + *sV + *sT + 2 * *sW + *sP;
+}
+
+// WY factor of an outer block of nbi inner 32-column blocks (xLARFT, blocked):
+// T_O = [[T_A, -T_A (V_A^H V_b) T_b], [0, T_b]] appended block by block, with
+// S = V_O^H V_O precomputed by one GEMM.  One CTA; T_O (row-major, ld QR_NBO)
+// in global memory (L2), Z = S[0:n0, n0:n0+32] T_b staged in shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, const T* Tin, T* TO, int jbo) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Z = reinterpret_cast<T*>(smem_raw);  // (QR_NBO - QR_NB) x (QR_NB + 1)
+  const int tid = threadIdx.x;
+  const int nbi = (jbo + QR_NB - 1) / QR_NB;
+  for (int idx = tid; idx < QR_NBO * QR_NBO; idx += blockDim.x) {
+    const int r = idx / QR_NBO, c = idx % QR_NBO;
+    const int br = r / QR_NB, bc = c / QR_NB;
+    TO[idx] = (br == bc && r < jbo && c < jbo) ? Tin[(size_t)br * QR_NB * QR_NB + (r % QR_NB) * QR_NB + (c % QR_NB)]
+                                               : Scalar<T>::zero();
+  }
+  __syncthreads();
+  for (int b = 1; b < nbi; ++b) {
+    const int n0 = b * QR_NB, w = min(QR_NB, jbo - n0);
+    const T* Tb = Tin + (size_t)b * QR_NB * QR_NB;
+    for (int idx = tid; idx < n0 * w; idx += blockDim.x) {  // Z = S[0:n0, n0:n0+w] T_b (T_b upper triangular)
+      const int r = idx / w, c = idx % w;
+      T z = Scalar<T>::zero();
+      for (int q = 0; q <= c; ++q) z = add(z, mul(S[(size_t)r * lds + n0 + q], Tb[q * QR_NB + c]));
+      Z[r * (QR_NB + 1) + c] = z;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n0 * w; idx += blockDim.x) {  // T_O[0:n0, n0:n0+w] = -T_O[0:n0, 0:n0] Z
+      const int r = idx / w, c = idx % w;
+      T acc = Scalar<T>::zero();
+      for (int q = r; q < n0; ++q) acc = add(acc, mul(TO[(size_t)r * QR_NBO + q], Z[q * (QR_NB + 1) + c]));
+      TO[(size_t)r * QR_NBO + n0 + c] = sub(Scalar<T>::zero(), acc);
+    }
+    __syncthreads();
+  }
 }
 
 template <typename T>
@@ -1296,6 +1335,60 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   copy_in_kernel<T><<<dim3(blocks_for((long long)m * n), chains), 256, 0, s>>>(static_cast<const T*>(p.A), p.sA, A,
                                                                              w.sA, (long long)m * n);
   ++nl;
+  // two-level blocking: 32-column panels, trailing/Q updates per 128-column outer block (K = 128)
+  static const bool two_level = [] {
+    const char* ev = std::getenv("TTG_QR_2L");
+    return !(ev && ev[0] == '0');
+  }();
+  const int nblk_in = (k + QR_NB - 1) / QR_NB;
+  T* To_all = Tt + (size_t)nblk_in * QR_NB * QR_NB;  // outer WY factors, QR_NBO x QR_NBO each
+  T* Sbuf = To_all + (size_t)((k + QR_NBO - 1) / QR_NBO) * QR_NBO * QR_NBO;
+  if (two_level) {
+    if ((e = cudaMemsetAsync(V, 0, (size_t)w.sV * (chains - 1) * sizeof(T) + (size_t)m * k * sizeof(T), s)) !=
+        cudaSuccess)
+      return e;
+    e = cudaFuncSetAttribute(t_combine_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T)));
+    if (e != cudaSuccess) return e;
+  }
+  // outer block: S = V_O^H V_O, T_O (t_combine); far columns [jend, n) -= V_O T_O^H V_O^H A
+  auto outer = [&](int J0, int jend, bool far) -> cudaError_t {
+    const int jbo = jend - J0, mpo = m - J0;
+    T* To = To_all + (size_t)(J0 / QR_NBO) * QR_NBO * QR_NBO;
+    GemmParams gs{V + (size_t)J0 * k + J0, V + (size_t)J0 * k + J0, Sbuf, w.sV, w.sV, w.sT, dconst(jbo), dconst(jbo),
+                  dconst(mpo), nullptr, 0, nullptr, 1.0, 0};
+    gs.lda = k;
+    gs.ldb = k;
+    gs.ldc = jbo;
+    cudaError_t e2;
+    if ((e2 = gemm<T>(gs, OP_C, OP_N, jbo, jbo, chains, s, mpo)) != cudaSuccess) return e2;
+    for (int c = 0; c < chains; ++c)
+      t_combine_kernel<T><<<1, 256, (QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T), s>>>(
+          Sbuf + (size_t)c * w.sT, jbo, Tt + (size_t)c * w.sT + (size_t)(J0 / QR_NB) * QR_NB * QR_NB,
+          To + (size_t)c * w.sT, jbo);
+    nl += 1 + chains;
+    const int nt = n - jend;
+    if (!far || nt <= 0) return cudaGetLastError();
+    GemmParams g1{V + (size_t)J0 * k + J0, A + (size_t)J0 * n + jend, w.W1, w.sV, w.sA, w.sW, dconst(jbo), dconst(nt),
+                  dconst(mpo), nullptr, 0, nullptr, 1.0, 0};
+    g1.lda = k;
+    g1.ldb = n;
+    g1.ldc = nt;
+    if ((e2 = gemm<T>(g1, OP_C, OP_N, jbo, nt, chains, s, mpo)) != cudaSuccess) return e2;
+    GemmParams g2{To, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jbo), dconst(nt), dconst(jbo), nullptr, 0, nullptr, 1.0, 0};
+    g2.lda = QR_NBO;
+    g2.ldb = nt;
+    g2.ldc = nt;
+    if ((e2 = gemm<T>(g2, OP_C, OP_N, jbo, nt, chains, s)) != cudaSuccess) return e2;
+    GemmParams g3{V + (size_t)J0 * k + J0, w.W2, A + (size_t)J0 * n + jend, w.sV, w.sW, w.sA, dconst(mpo), dconst(nt),
+                  dconst(jbo), nullptr, 0, nullptr, -1.0, 1};
+    g3.lda = k;
+    g3.ldb = nt;
+    g3.ldc = n;
+    if ((e2 = gemm<T>(g3, OP_N, OP_N, mpo, nt, chains, s)) != cudaSuccess) return e2;
+    nl += 3;
+    return cudaSuccess;
+  };
   const size_t panel_bytes_max = (size_t)m * QR_NB * sizeof(T);
   const size_t smem_limit = 200 * 1024;
   e = cudaFuncSetAttribute(qr_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
@@ -1387,7 +1480,9 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
           Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.sT, static_cast<T*>(w.P), w.sP);
     ++nl;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const int nt = n - j0 - jb;
+    const int J0 = (j0 / QR_NBO) * QR_NBO;
+    const int jend = two_level ? (J0 + QR_NBO < k ? J0 + QR_NBO : k) : n;  // inner updates stop at the block end
+    const int nt = jend - j0 - jb;
     if (nt > 0) {
       // W1 = V^H A_trail (jb x nt)
       GemmParams g1{V + (size_t)j0 * k + j0, A + (size_t)j0 * n + j0 + jb, w.W1, w.sV, w.sA, w.sW, dconst(jb), dconst(nt),
@@ -1412,6 +1507,8 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       if ((e = gemm<T>(g3, OP_N, OP_N, mp, nt, chains, s)) != cudaSuccess) return e;
       nl += 3;
     }
+    if (two_level && j0 + jb == jend && (jend < n || p.Q))
+      if ((e = outer(J0, jend, jend < n)) != cudaSuccess) return e;
   }
   if (coop_part) cudaFreeAsync(coop_part, s);
   upper_kernel<T><<<dim3(blocks_for((long long)k * n), chains), 256, 0, s>>>(A, w.sA, n, static_cast<T*>(p.R), p.sR, k);
@@ -1422,10 +1519,11 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   }
   eye_kernel<T><<<dim3(blocks_for((long long)m * k), chains), 256, 0, s>>>(Q, p.sQ, m, k);
   nl += 2;
-  const int nblk = (k + QR_NB - 1) / QR_NB;
+  const int NBQ = two_level ? QR_NBO : QR_NB;
+  const int nblk = (k + NBQ - 1) / NBQ;
   for (int b = nblk - 1; b >= 0; --b) {
-    const int j0 = b * QR_NB;
-    const int jb = (k - j0) < QR_NB ? (k - j0) : QR_NB;
+    const int j0 = b * NBQ;
+    const int jb = (k - j0) < NBQ ? (k - j0) : NBQ;
     const int mp = m - j0, kq = k - j0;
     // W1 = V^H Q_sub (jb x kq)
     GemmParams g1{V + (size_t)j0 * k + j0, Q + (size_t)j0 * k + j0, w.W1, w.sV, p.sQ, w.sW, dconst(jb), dconst(kq),
@@ -1435,9 +1533,9 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     g1.ldc = kq;
     if ((e = gemm<T>(g1, OP_C, OP_N, jb, kq, chains, s, mp)) != cudaSuccess) return e;
     // W2 = T W1
-    GemmParams g2{Tt + (size_t)b * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(kq), dconst(jb),
-                  nullptr, 0, nullptr, 1.0, 0};
-    g2.lda = QR_NB;
+    GemmParams g2{two_level ? To_all + (size_t)b * QR_NBO * QR_NBO : Tt + (size_t)b * QR_NB * QR_NB, w.W1, w.W2, w.sT,
+                  w.sW, w.sW, dconst(jb), dconst(kq), dconst(jb), nullptr, 0, nullptr, 1.0, 0};
+    g2.lda = NBQ;
     g2.ldb = kq;
     g2.ldc = kq;
     if ((e = gemm<T>(g2, OP_N, OP_N, jb, kq, chains, s)) != cudaSuccess) return e;

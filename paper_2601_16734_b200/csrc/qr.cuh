@@ -68,13 +68,14 @@ namespace ttg {
 struct QrBlockedWork {
   void* A;   // m x n working copy
   void* V;   // m x k unit lower-trapezoidal reflectors
-  void* T;   // ceil(k/32) x 32 x 32 WY factors
-  void* W1;  // 32 x n
-  void* W2;  // 32 x n
+  void* T;   // ceil(k/32) x 32 x 32 inner + (ceil(k/128) + 1) x 128 x 128 outer WY factors / S scratch
+  void* W1;  // 128 x n
+  void* W2;  // 128 x n
   void* P;   // panel scratch m x 32 (global fallback of the panel kernel)
   long long sA, sV, sT, sW, sP;  // per-chain strides
 };
 constexpr int QR_NB = 32;
+constexpr int QR_NBO = 128;  // outer block: trailing and Q updates use K = 128 (two-level blocking)
 template <typename T> size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t* sW, size_t* sP);
 // dst (cols x rows) = src^H (rows x cols), row-major, batched
 template <typename T>
