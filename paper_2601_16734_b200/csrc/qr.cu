@@ -1290,10 +1290,14 @@ size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t
 // S = V_O^H V_O precomputed by one GEMM.  One CTA; T_O (row-major, ld QR_NBO)
 // in global memory (L2), Z = S[0:n0, n0:n0+32] T_b staged in shared memory.
 template <typename T>
-__global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, const T* Tin, T* TO, int jbo) {
+__global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, const T* Tin, T* TO, int jbo,
+                                                        long long stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Z = reinterpret_cast<T*>(smem_raw);  // (QR_NBO - QR_NB) x (QR_NB + 1)
   const int tid = threadIdx.x;
+  S += stride * blockIdx.x;  // one CTA per chain
+  Tin += stride * blockIdx.x;
+  TO += stride * blockIdx.x;
   const int nbi = (jbo + QR_NB - 1) / QR_NB;
   for (int idx = tid; idx < QR_NBO * QR_NBO; idx += blockDim.x) {
     const int r = idx / QR_NBO, c = idx % QR_NBO;
@@ -1362,11 +1366,9 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     gs.ldc = jbo;
     cudaError_t e2;
     if ((e2 = gemm<T>(gs, OP_C, OP_N, jbo, jbo, chains, s, mpo)) != cudaSuccess) return e2;
-    for (int c = 0; c < chains; ++c)
-      t_combine_kernel<T><<<1, 256, (QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T), s>>>(
-          Sbuf + (size_t)c * w.sT, jbo, Tt + (size_t)c * w.sT + (size_t)(J0 / QR_NB) * QR_NB * QR_NB,
-          To + (size_t)c * w.sT, jbo);
-    nl += 1 + chains;
+    t_combine_kernel<T><<<chains, 256, (QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T), s>>>(
+        Sbuf, jbo, Tt + (size_t)(J0 / QR_NB) * QR_NB * QR_NB, To, jbo, w.sT);
+    nl += 2;
     const int nt = n - jend;
     if (!far || nt <= 0) return cudaGetLastError();
     GemmParams g1{V + (size_t)J0 * k + J0, A + (size_t)J0 * n + jend, w.W1, w.sV, w.sA, w.sW, dconst(jbo), dconst(nt),
