@@ -1340,10 +1340,12 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
                                                                              w.sA, (long long)m * n);
   ++nl;
   // two-level blocking: 32-column panels, trailing/Q updates per 128-column outer block (K = 128)
-  static const bool two_level = [] {
+  // (complex: measured slower on C3, so the 32-column updates stay)
+  static const int two_level_env = [] {
     const char* ev = std::getenv("TTG_QR_2L");
-    return !(ev && ev[0] == '0');
+    return ev ? std::atoi(ev) : -1;
   }();
+  const bool two_level = two_level_env >= 0 ? two_level_env != 0 : !Scalar<T>::is_complex;
   const int nblk_in = (k + QR_NB - 1) / QR_NB;
   T* To_all = Tt + (size_t)nblk_in * QR_NB * QR_NB;  // outer WY factors, QR_NBO x QR_NBO each
   T* Sbuf = To_all + (size_t)((k + QR_NBO - 1) / QR_NBO) * QR_NBO * QR_NBO;
