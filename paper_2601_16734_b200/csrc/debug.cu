@@ -54,6 +54,10 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   int hb[4] = {m, n, 0, 0};
   cudaMemcpy(bonds.p, hb, sizeof hb, cudaMemcpyHostToDevice);
   SvdParams p{};
+  {
+    const char* e = getenv("TTG_SVD_EARLY");
+    p.no_early = (e && e[0] == '0') ? 1 : 0;
+  }
   p.theta = th.p;
   p.M = dbond(0);
   p.N = dbond(1);

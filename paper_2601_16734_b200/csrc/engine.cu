@@ -281,6 +281,11 @@ struct Engine {
          int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work,
          const Warm& w = Warm(), bool no_pre = false) {
     SvdParams p{};
+    static const int no_early = [] {
+      const char* e = getenv("TTG_SVD_EARLY");
+      return (e && e[0] == '0') ? 1 : 0;
+    }();
+    p.no_early = no_early;
     p.theta_pre = w.pre;
     p.s_pre = w.s_pre;
     p.frame_in = w.fin;

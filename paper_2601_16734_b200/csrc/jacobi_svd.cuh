@@ -31,6 +31,7 @@ struct SvdParams {
   long long s_work;
   int* sweeps_out;    // nullable: Jacobi sweeps executed per chain (diagnostics)
   double tol_rot;     // rotation threshold |a^H b| > tol_rot |a||b|; 0 = default l*eps
+  int no_early;       // 1: iterate until a sweep rotates nothing (no early stop, see early_stop2)
   // Warm start.  theta_pre = theta F for mode 0 (F = V frame of the previous
   // split at this bond) or F^H theta for mode 1 (F = U frame); it has the same
   // singular values and the same isometry as theta.  It is used only when
