@@ -235,7 +235,103 @@ template <int NV> __device__ __forceinline__ int treduce_index(int lane) {
 // lanes that differ only in these bits hold the same value
 template <int NV> __host__ __device__ constexpr int treduce_dup_mask() { return 32 / NV - 1; }
 
-template <typename T, int RT, int NB>
+// All-warp panel factorisation (real, NB <= 16): the panel's NB columns are
+// spread over the lanes (two lanes per column, lane = 2c + h) and its rows over
+// the 8 warps (lane half h of warp w holds rows 8 (2r + h) + w), so every
+// warp holds a row slab of every column.  Per column ONE CTA reduction: each
+// lane forms the partial x^H a_c over its rows (x = the pivot column, fetched
+// from the lanes of the same warp that own it, which hold the same rows), the
+// two halves combine by one shuffle and the 8 warp partials meet in shared
+// memory behind one barrier; every lane then forms the same reflector (xLARFG)
+// and updates its rows.  Row j + 1 of the panel (the next alpha and the
+// a_c(j) terms) is published through shared memory for the next column; all
+// scratch is double-buffered by column parity, so one barrier per column
+// suffices.  Replaces the one-warp register panel, during which the other
+// seven warps idled (profiles/r01_qrs.hot.txt: 42% of the stall samples).
+template <int RS, int NB>
+__device__ __forceinline__ void panel_allwarps(double* Wk, double* Vs, int lw, int l, int j0, int nb, double* taus,
+                                               double (*part)[QRS_NW][NB], double (*srow)[NB]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane >> 1, h = lane & 1;
+  const bool cv = c < nb;
+  double a[RS];
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const int i = 8 * (2 * r + h) + warp;
+    a[r] = (cv && i < l) ? Wk[(long long)(j0 + c) * lw + i] : 0.0;
+    if (cv && i == j0) srow[0][c] = a[r];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int jj = 0; jj < nb; ++jj) {
+    const int j = j0 + jj, buf = jj & 1;
+    // pivot column values at my rows (lanes 2 jj + h hold the same rows)
+    double x[RS];
+    double q = 0.0;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      x[r] = __shfl_sync(0xffffffffu, a[r], 2 * jj + h);
+      const int i = 8 * (2 * r + h) + warp;
+      if (i > j && i < l) q = fma(x[r], a[r], q);
+    }
+    q += __shfl_xor_sync(0xffffffffu, q, 1);
+    if (h == 0 && cv) part[buf][warp][c] = q;
+    __syncthreads();
+    double qc = 0.0, xn2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < QRS_NW; ++w) {
+      qc += cv ? part[buf][w][c] : 0.0;
+      xn2 += part[buf][w][jj];
+    }
+    const double alpha = srow[buf][jj];
+    double tau = 0.0, beta = alpha, sc = 0.0;
+    if (xn2 != 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    if (c > jj && cv) {
+      // v^H a_c = a_c(j) + sc * x^H a_c (v_j = 1, v_i = sc x_i below)
+      const double f = tau * fma(sc, qc, srow[buf][c]);
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        const int i = 8 * (2 * r + h) + warp;
+        if (i > j && i < l)
+          a[r] = fma(-f, x[r] * sc, a[r]);
+        else if (i == j)
+          a[r] -= f;
+      }
+    } else if (c == jj) {
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        const int i = 8 * (2 * r + h) + warp;
+        if (i > j && i < l)
+          a[r] *= sc;
+        else if (i == j)
+          a[r] = beta;
+      }
+    }
+    // row j + 1 of the remaining columns for the next column step
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      const int i = 8 * (2 * r + h) + warp;
+      if (i == j + 1 && cv) srow[buf ^ 1][c] = a[r];
+    }
+    if (threadIdx.x == 0) taus[jj] = tau;
+  }
+  // factored panel back to Wk (R on/above the diagonal, v below) and the explicit V to Vs
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const int i = 8 * (2 * r + h) + warp;
+    if (cv && i < l) {
+      const int jc = j0 + c;
+      Wk[(long long)jc * lw + i] = a[r];
+      Vs[(long long)c * lw + i] = i > jc ? a[r] : (i == jc ? 1.0 : 0.0);
+    }
+  }
+}
+
+template <typename T, int RT, int NB, bool ALLW>
 __global__ void __launch_bounds__(QRS_THREADS, 1)
     qr_small_kernel(const T* A, long long sA, DimExpr Md, DimExpr Nd, int trans, int* bonds, int ld, int out_idx,
                     T* Q, long long sQ, T* RH, long long sRH, const ChainState* st) {
@@ -270,7 +366,11 @@ __global__ void __launch_bounds__(QRS_THREADS, 1)
   for (int j0 = 0, p = 0; j0 < r0; j0 += NB, ++p) {
     const int nb = min(NB, r0 - j0);
     T* Tp = Tall + (long long)p * NB * NB;
-    if (warp == 0) {
+    if constexpr (ALLW) {
+      __shared__ double s_part[2][QRS_NW][NB];
+      __shared__ double s_row[2][NB];
+      panel_allwarps<2 * RT, NB>(Wk, Vs, lw, l, j0, nb, taus, s_part, s_row);
+    } else if (warp == 0) {
       // ---- panel factorisation in registers: lane holds rows j0 + lane + 32 t of
       // a rolling window of NB columns (a[t][0] = the current column; the window
       // shifts left after every column, so the loop body is the same code for all
@@ -470,19 +570,32 @@ __global__ void __launch_bounds__(QRS_THREADS, 1)
   }
 }
 
+bool qr_panel_allwarps() {
+  static const bool on = [] {
+    const char* e = std::getenv("TTG_QR_PANEL_ALL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename T, int RT, int NB>
 cudaError_t launch_small(const void* A, long long sA, DimExpr M, DimExpr N, int trans, int* bonds, int ld, int out_idx,
                          void* Q, long long sQ, void* RH, long long sRH, int lmax, int kmax, const ChainState* st,
                          int chains, cudaStream_t s) {
   const SmallLayout L = small_layout(lmax, kmax, NB);
   const size_t bytes = (size_t)L.total * sizeof(T);
-  cudaError_t e =
-      cudaFuncSetAttribute(qr_small_kernel<T, RT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return e;
-  qr_small_kernel<T, RT, NB><<<chains, QRS_THREADS, bytes, s>>>(static_cast<const T*>(A), sA, M, N, trans, bonds, ld,
-                                                               out_idx, static_cast<T*>(Q), sQ, static_cast<T*>(RH),
-                                                               sRH, st);
-  return cudaGetLastError();
+  constexpr bool CAN_ALLW = !Scalar<T>::is_complex && NB == 16;  // two lanes per panel column
+  auto go = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<chains, QRS_THREADS, bytes, s>>>(static_cast<const T*>(A), sA, M, N, trans, bonds, ld, out_idx,
+                                           static_cast<T*>(Q), sQ, static_cast<T*>(RH), sRH, st);
+    return cudaGetLastError();
+  };
+  if constexpr (CAN_ALLW) {
+    if (qr_panel_allwarps()) return go(qr_small_kernel<T, RT, NB, true>);
+  }
+  return go(qr_small_kernel<T, RT, NB, false>);
 }
 
 }  // namespace
