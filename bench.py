@@ -511,7 +511,7 @@ def run_ours_batch(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out, reps, allst = step(ttlab.DeviceMPS.from_batch(chains, ctx=ctx))
-        res = [out.to_tensors(c) for c in range(len(chains))]
+        res = out.to_tensors_batch()
         t_e2e += time.perf_counter() - t0
         e2e_sweeps += int(allst[:, 2].sum().item())
         d2h = sum(a.nbytes for ch in res for a in ch)

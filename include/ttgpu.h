@@ -125,6 +125,10 @@ ttg_status ttg_mps_info(const ttg_dmps* m, int chain, int* n, int* dtype, int* c
                         double* error, int* center);
 /* Copy chain `chain` to caller-allocated host buffers sized from ttg_mps_info. */
 ttg_status ttg_mps_download(ttg_ctx* ctx, const ttg_dmps* m, int chain, void* const* sites);
+/* Copy every chain of the batch to caller-allocated host buffers: sites[c * n + k] receives site k
+ * of chain c (shapes from ttg_mps_info).  Batches stream through pinned staging buffers (one D2H
+ * per staging chunk instead of one per chain and site). */
+ttg_status ttg_mps_download_batch(ttg_ctx* ctx, const ttg_dmps* m, void* const* sites);
 /* Device pointer of site k of chain `chain` and its element count (for zero-copy readers). */
 ttg_status ttg_mps_site_ptr(const ttg_dmps* m, int chain, int k, void** ptr, int64_t* elems);
 

@@ -59,6 +59,7 @@ SIGNATURES = {
                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                C.POINTER(C.c_int)]),
     "ttg_mps_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "ttg_mps_download_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ttg_mps_site_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "ttg_mpo_upload": (C.c_int, [C.c_void_p, C.POINTER(ttg_mpo_view), C.POINTER(C.c_void_p)]),
     "ttg_mpo_free": (None, [C.c_void_p]),

@@ -1091,6 +1091,15 @@ ttg_status ttg_profile_read(ttg_ctx* ctx, int cls, int64_t* launches, double* ms
   return TTG_OK;
 }
 
+// pinned staging buffers of the context (shared with the TTLAB1 I/O path), allocated on first use
+static size_t mps_stage_bytes() { return size_t(32) << 20; }
+static void mps_stage_init(ttg_ctx* ctx) {
+  for (int i = 0; i < 2; ++i) {
+    if (!ctx->stage[i]) CK(cudaMallocHost(&ctx->stage[i], mps_stage_bytes()));
+    if (!ctx->stage_ev[i]) CK(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+  }
+}
+
 ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, ttg_dmps** out) {
   return guarded(ctx, [&] {
     if (!views || !out || count < 1) throw Error{TTG_INVALID, "null argument"};
@@ -1118,10 +1127,44 @@ ttg_status ttg_mps_upload(ttg_ctx* ctx, const ttg_mps_view* views, int count, tt
       const ttg_mps_view& v = views[c];
       m->error[c] = v.error;
       for (int k = 0; k <= n; ++k) m->bonds[(size_t)c * (n + 1) + k] = (int)v.bonds[k];
+    }
+    // Batches go through the two pinned staging buffers: the chains' site-k tensors are packed
+    // in the device layout (chain c at c * cap[k]) and cross PCIe as one copy per staging
+    // chunk, the packing of chunk i+1 overlapping the DMA of chunk i.  Single chains and
+    // tensors larger than a staging buffer are copied directly.
+    const bool staged = count > 1 && [&] {
+      for (int k = 0; k < n; ++k)
+        if ((size_t)cap[k] * es > mps_stage_bytes()) return false;
+      return true;
+    }();
+    if (staged) {
+      mps_stage_init(ctx);
+      int cur = 0;
       for (int k = 0; k < n; ++k) {
-        const size_t bytes = (size_t)(v.bonds[k] * v.phys[k] * v.bonds[k + 1]) * es;
-        CK(cudaMemcpyAsync(static_cast<char*>(m->site[k]) + (size_t)c * cap[k] * es, v.sites[k], bytes,
-                           cudaMemcpyHostToDevice, ctx->stream));
+        const size_t cb = (size_t)cap[k] * es;
+        const int per = (int)std::max<size_t>(1, mps_stage_bytes() / cb);
+        for (int c0 = 0; c0 < count; c0 += per) {
+          const int c1 = std::min(count, c0 + per);
+          CK(cudaEventSynchronize(ctx->stage_ev[cur]));
+          char* stg = static_cast<char*>(ctx->stage[cur]);
+          for (int c = c0; c < c1; ++c) {
+            const ttg_mps_view& v = views[c];
+            std::memcpy(stg + (size_t)(c - c0) * cb, v.sites[k], (size_t)(v.bonds[k] * v.phys[k] * v.bonds[k + 1]) * es);
+          }
+          CK(cudaMemcpyAsync(static_cast<char*>(m->site[k]) + (size_t)c0 * cb, stg, (size_t)(c1 - c0) * cb,
+                             cudaMemcpyHostToDevice, ctx->stream));
+          CK(cudaEventRecord(ctx->stage_ev[cur], ctx->stream));
+          cur ^= 1;
+        }
+      }
+    } else {
+      for (int c = 0; c < count; ++c) {
+        const ttg_mps_view& v = views[c];
+        for (int k = 0; k < n; ++k) {
+          const size_t bytes = (size_t)(v.bonds[k] * v.phys[k] * v.bonds[k + 1]) * es;
+          CK(cudaMemcpyAsync(static_cast<char*>(m->site[k]) + (size_t)c * cap[k] * es, v.sites[k], bytes,
+                             cudaMemcpyHostToDevice, ctx->stream));
+        }
       }
     }
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1180,6 +1223,54 @@ ttg_status ttg_mps_download(ttg_ctx* ctx, const ttg_dmps* m, int chain, void* co
                          cudaMemcpyDeviceToHost, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+ttg_status ttg_mps_download_batch(ttg_ctx* ctx, const ttg_dmps* m, void* const* sites) {
+  return guarded(ctx, [&] {
+    if (!m || !sites) throw Error{TTG_INVALID, "bad argument"};
+    const size_t es = esize(m->dtype);
+    const int n = m->n, count = m->count;
+    bool staged = count > 1;
+    for (int k = 0; k < n; ++k) staged = staged && (size_t)m->cap[k] * es <= mps_stage_bytes();
+    if (!staged) {
+      for (int c = 0; c < count; ++c)
+        for (int k = 0; k < n; ++k) {
+          const size_t bytes = (size_t)m->bond(c, k) * m->phys[k] * m->bond(c, k + 1) * es;
+          CK(cudaMemcpyAsync(sites[(size_t)c * n + k], static_cast<const char*>(m->site[k]) + (size_t)c * m->cap[k] * es,
+                             bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+      CK(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    // one D2H per staging chunk (chains [c0, c1) of site k in the device layout); the copy of
+    // the next chunk is in flight while the current one is scattered into the caller's buffers
+    mps_stage_init(ctx);
+    struct Chunk { int k, c0, c1; };
+    std::vector<Chunk> chunks;
+    for (int k = 0; k < n; ++k) {
+      const size_t cb = (size_t)m->cap[k] * es;
+      const int per = (int)std::max<size_t>(1, mps_stage_bytes() / cb);
+      for (int c0 = 0; c0 < count; c0 += per) chunks.push_back({k, c0, std::min(count, c0 + per)});
+    }
+    auto issue = [&](size_t i) {
+      const Chunk& q = chunks[i];
+      const size_t cb = (size_t)m->cap[q.k] * es;
+      CK(cudaMemcpyAsync(ctx->stage[i & 1], static_cast<const char*>(m->site[q.k]) + (size_t)q.c0 * cb,
+                         (size_t)(q.c1 - q.c0) * cb, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaEventRecord(ctx->stage_ev[i & 1], ctx->stream));
+    };
+    issue(0);
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      if (i + 1 < chunks.size()) issue(i + 1);
+      CK(cudaEventSynchronize(ctx->stage_ev[i & 1]));
+      const Chunk& q = chunks[i];
+      const size_t cb = (size_t)m->cap[q.k] * es;
+      const char* stg = static_cast<const char*>(ctx->stage[i & 1]);
+      for (int c = q.c0; c < q.c1; ++c)
+        std::memcpy(sites[(size_t)c * n + q.k], stg + (size_t)(c - q.c0) * cb,
+                    (size_t)m->bond(c, q.k) * m->phys[q.k] * m->bond(c, q.k + 1) * es);
+    }
   });
 }
 

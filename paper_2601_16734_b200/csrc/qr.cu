@@ -1289,22 +1289,29 @@ size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t
 // T_O = [[T_A, -T_A (V_A^H V_b) T_b], [0, T_b]] appended block by block, with
 // S = V_O^H V_O precomputed by one GEMM.  One CTA; T_O (row-major, ld QR_NBO)
 // in global memory (L2), Z = S[0:n0, n0:n0+32] T_b staged in shared memory.
+// T_O is upper triangular: it is built in shared memory with its upper triangle packed by rows
+// (row r holds columns r .. QR_NBO-1; 66 KB real, 132 KB complex) and written out once, so the
+// triangular products read shared memory instead of L2.
+__host__ __device__ constexpr int tri_off(int r) { return r * QR_NBO - r * (r - 1) / 2; }
+
 template <typename T>
 __global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, const T* Tin, T* TO, int jbo,
                                                         long long stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Z = reinterpret_cast<T*>(smem_raw);  // (QR_NBO - QR_NB) x (QR_NB + 1)
+  T* Z = reinterpret_cast<T*>(smem_raw);        // (QR_NBO - QR_NB) x (QR_NB + 1)
+  T* Tp = Z + (QR_NBO - QR_NB) * (QR_NB + 1);  // packed upper triangle of T_O
   const int tid = threadIdx.x;
   S += stride * blockIdx.x;  // one CTA per chain
   Tin += stride * blockIdx.x;
   TO += stride * blockIdx.x;
   const int nbi = (jbo + QR_NB - 1) / QR_NB;
-  for (int idx = tid; idx < QR_NBO * QR_NBO; idx += blockDim.x) {
-    const int r = idx / QR_NBO, c = idx % QR_NBO;
-    const int br = r / QR_NB, bc = c / QR_NB;
-    TO[idx] = (br == bc && r < jbo && c < jbo) ? Tin[(size_t)br * QR_NB * QR_NB + (r % QR_NB) * QR_NB + (c % QR_NB)]
-                                               : Scalar<T>::zero();
-  }
+  for (int r = tid / 32; r < QR_NBO; r += blockDim.x / 32)  // diagonal blocks T_b, zero elsewhere
+    for (int c = r + (tid & 31); c < QR_NBO; c += 32) {
+      const int br = r / QR_NB, bc = c / QR_NB;
+      Tp[tri_off(r) + c - r] = (br == bc && r < jbo && c < jbo)
+                                   ? Tin[(size_t)br * QR_NB * QR_NB + (r % QR_NB) * QR_NB + (c % QR_NB)]
+                                   : Scalar<T>::zero();
+    }
   __syncthreads();
   for (int b = 1; b < nbi; ++b) {
     const int n0 = b * QR_NB, w = min(QR_NB, jbo - n0);
@@ -1318,12 +1325,22 @@ __global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, con
     __syncthreads();
     for (int idx = tid; idx < n0 * w; idx += blockDim.x) {  // T_O[0:n0, n0:n0+w] = -T_O[0:n0, 0:n0] Z
       const int r = idx / w, c = idx % w;
+      const T* row = Tp + tri_off(r) - r;  // row[q] = T_O[r][q], q >= r
       T acc = Scalar<T>::zero();
-      for (int q = r; q < n0; ++q) acc = add(acc, mul(TO[(size_t)r * QR_NBO + q], Z[q * (QR_NB + 1) + c]));
-      TO[(size_t)r * QR_NBO + n0 + c] = sub(Scalar<T>::zero(), acc);
+      for (int q = r; q < n0; ++q) acc = add(acc, mul(row[q], Z[q * (QR_NB + 1) + c]));
+      Tp[tri_off(r) + n0 + c - r] = sub(Scalar<T>::zero(), acc);
     }
     __syncthreads();
   }
+  for (int idx = tid; idx < QR_NBO * QR_NBO; idx += blockDim.x) {
+    const int r = idx / QR_NBO, c = idx % QR_NBO;
+    TO[idx] = c >= r ? Tp[tri_off(r) + c - r] : Scalar<T>::zero();
+  }
+}
+
+template <typename T>
+constexpr size_t t_combine_smem() {
+  return ((size_t)(QR_NBO - QR_NB) * (QR_NB + 1) + (size_t)tri_off(QR_NBO)) * sizeof(T);
 }
 
 template <typename T>
@@ -1340,14 +1357,15 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
                                                                              w.sA, (long long)m * n);
   ++nl;
   // two-level blocking: 32-column panels, trailing/Q updates per 128-column outer block (K = 128)
-  // (complex: measured slower on C3, so the 32-column updates stay)
   static const int two_level_env = [] {
     const char* ev = std::getenv("TTG_QR_2L");
     return ev ? std::atoi(ev) : -1;
   }();
   // (narrow matrices: the outer T factor (t_combine) costs more than the K = 128 updates save; C2's
-  // 384 x 192 exact-pass QRs measured 1.5 ms per call faster without it)
-  const bool two_level = two_level_env >= 0 ? two_level_env != 0 : (!Scalar<T>::is_complex && k >= 512);
+  // 384 x 192 exact-pass QRs measured 1.5 ms per call faster without it.  Complex: C3 3.36 -> 2.57 s
+  // once t_combine keeps T_O in shared memory; the rank-32 updates stream the trailing matrix
+  // from HBM four times as often)
+  const bool two_level = two_level_env >= 0 ? two_level_env != 0 : k >= 512;
   const int nblk_in = (k + QR_NB - 1) / QR_NB;
   T* To_all = Tt + (size_t)nblk_in * QR_NB * QR_NB;  // outer WY factors, QR_NBO x QR_NBO each
   T* Sbuf = To_all + (size_t)((k + QR_NBO - 1) / QR_NBO) * QR_NBO * QR_NBO;
@@ -1356,7 +1374,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
         cudaSuccess)
       return e;
     e = cudaFuncSetAttribute(t_combine_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T)));
+                             (int)t_combine_smem<T>());
     if (e != cudaSuccess) return e;
   }
   // outer block: S = V_O^H V_O, T_O (t_combine); far columns [jend, n) -= V_O T_O^H V_O^H A
@@ -1370,7 +1388,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     gs.ldc = jbo;
     cudaError_t e2;
     if ((e2 = gemm<T>(gs, OP_C, OP_N, jbo, jbo, chains, s, mpo)) != cudaSuccess) return e2;
-    t_combine_kernel<T><<<chains, 256, (QR_NBO - QR_NB) * (QR_NB + 1) * sizeof(T), s>>>(
+    t_combine_kernel<T><<<chains, 256, t_combine_smem<T>(), s>>>(
         Sbuf, jbo, Tt + (size_t)(J0 / QR_NB) * QR_NB * QR_NB, To, jbo, w.sT);
     nl += 2;
     const int nt = n - jend;

@@ -281,6 +281,20 @@ class DeviceMPS:
         self.ctx.check(lib.ttg_mps_download(self.ctx.handle, self.handle, chain, ptrs))
         return arrs
 
+    def to_tensors_batch(self) -> List[List[np.ndarray]]:
+        """Every chain of the batch (ttg_mps_download_batch: pinned staging, one copy per chunk)."""
+        first = self.info(0)
+        dt = _np_dtype(first["dtype"])
+        out, ptrs = [], []
+        for c in range(first["count"]):
+            inf = first if c == 0 else self.info(c)
+            b, p = inf["bonds"], inf["phys"]
+            arrs = [np.empty((b[k], p[k], b[k + 1]), dtype=dt) for k in range(inf["n"])]
+            out.append(arrs)
+            ptrs += [a.ctypes.data for a in arrs]
+        self.ctx.check(lib.ttg_mps_download_batch(self.ctx.handle, self.handle, (C.c_void_p * len(ptrs))(*ptrs)))
+        return out
+
     def site_ptr(self, chain: int, k: int):
         ptr, n = C.c_void_p(), C.c_int64()
         if lib.ttg_mps_site_ptr(self.handle, chain, k, C.byref(ptr), C.byref(n)) != _lib.TTG_OK:

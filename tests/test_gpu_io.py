@@ -111,3 +111,23 @@ def test_container_errors(tmp_path):
     (tmp_path / "mis").write_bytes(bytes(blob))
     with pytest.raises((t.ShapeError, t.NumericError)):
         t.load_mps(tmp_path / "mis")
+
+
+@pytest.mark.gpu
+def test_batch_upload_download_staged():
+    """Batched upload/download through the pinned staging buffers (ttg_mps_upload with count > 1,
+    ttg_mps_download_batch): ragged bonds per chain (padding in the device layout), more chains
+    than one staging chunk holds, bit-exact round trip, same as the per-chain download."""
+    t = T()
+    chains = [I.random_mps(12, 2, 8 + (c % 5) * 8, 900 + c) for c in range(37)]
+    big = [I.random_mps(20, 2, 512, 990 + c) for c in range(12)]  # 4 MB sites: 8 per 32 MB chunk
+    for batch in (chains, big):
+        d = t.DeviceMPS.from_batch(batch)
+        got = d.to_tensors_batch()
+        assert len(got) == len(batch)
+        for c, (g, ref) in enumerate(zip(got, batch)):
+            assert len(g) == len(ref)
+            for a, b in zip(g, ref):
+                assert a.shape == b.shape and np.array_equal(a, b)
+            for a, b in zip(d.to_tensors(c), g):
+                assert np.array_equal(a, b)
