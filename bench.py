@@ -246,7 +246,14 @@ def _workload_desc(cfg):
     return f"{cfg.name}: n={cfg.n} d={cfg.d} chi={cfg.chi} f64 MPS (seed {cfg.seed}+1000*rank), " + tail
 
 
-def _roofline(prof):
+# DRAM bytes per launch of the dominant SVD kernel (dram__bytes_read.sum + dram__bytes_write.sum,
+# ncu --clock-control none, profiles/r01_dram_svd.txt): the split matrices stay L2-resident, so
+# traffic is about one read of the matrix per launch
+_SVD_TRAFFIC = {"C2": {"kernel": "jacobi_cluster_kernel<double,16,8,128,2>", "bytes": 204117},
+                "C4": {"kernel": "jacobi_grid_kernel<double,4,4,256,1>", "bytes": 9784448}}
+
+
+def _roofline(prof, cfg_name=None):
     """Roofline of the dominant kernel class of a profiled call (CUDA events around
     every launch, executed flops from the live bond table)."""
     dom = max(("gemm", "svd", "qr"), key=lambda k: prof[k]["ms"])
@@ -257,7 +264,9 @@ def _roofline(prof):
         "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)", "svd": "ttg::jacobi_svd_kernel",
                    "qr": "ttg::qr_kernel"}[dom],
         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+        "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+        "traffic": (_SVD_TRAFFIC[cfg_name]["bytes"] if dom == "svd" and cfg_name in _SVD_TRAFFIC else None),
+        "traffic_unit": "bytes per launch of the dominant kernel (ncu dram__bytes_read+write)",
         "per_launch": {"launches_per_step": p["launches"], "avg_us": 1e3 * p["ms"] / max(1, p["launches"]),
                        "flops_per_launch": p["flops"] / max(1, p["launches"])},
         "share_of_step": {k: v["ms"] / max(1e-9, sum(x["ms"] for x in prof.values())) for k, v in prof.items()},
@@ -372,7 +381,7 @@ def run_ours(args):
         _call(ttlab, cfg, mpsd, Wd, strat)
         prof = ctx.profile_read()
         ctx.profile_enable(False)
-        roofline = _roofline(prof)
+        roofline = _roofline(prof, cfg.name)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -527,7 +536,7 @@ def run_ours_batch(args):
         step(batch)
         prof = ctx.profile_read()
         ctx.profile_enable(False)
-    roofline = _roofline(prof) if prof else None
+    roofline = _roofline(prof, cfg.name) if prof else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1

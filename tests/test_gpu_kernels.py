@@ -133,6 +133,27 @@ def test_jacobi_svd_random(dtype, shape, mode, svd_impl):
         assert np.abs((th @ iso.conj().T) @ iso - th).max() < 1e-12 * ref[0]
 
 
+@pytest.mark.parametrize("dtype,shape", [(np.float64, (600, 520)), (np.float64, (1000, 700)), (np.float64, (1024, 1024)),
+                                         (np.complex128, (480, 300)), (np.complex128, (300, 480))])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_jacobi_svd_grid_large(dtype, shape, mode, monkeypatch):
+    """Grid-cooperative block Jacobi at the C3/C4 split sizes (rows split over 2-CTA clusters)."""
+    monkeypatch.setenv("TTG_DEBUG_SVD_GRID", "1")
+    m, n = shape
+    rng = np.random.default_rng(m + 3 * n)
+    th = rng.standard_normal((m, n))
+    if dtype == np.complex128:
+        th = th + 1j * rng.standard_normal((m, n))
+    iso, sv, r, e2 = _svd(th, mode)
+    ref = np.linalg.svd(th, compute_uv=False)
+    assert np.abs(sv - ref).max() <= 1e-12 * ref[0]
+    assert r == min(m, n)
+    if mode == 0:
+        assert np.abs(iso.conj().T @ iso - np.eye(r)).max() < 1e-12
+    else:
+        assert np.abs(iso @ iso.conj().T - np.eye(r)).max() < 1e-12
+
+
 def test_svd_kat_identity():
     """test_core.cpp:74-90: theta = I/sqrt(2)."""
     th = np.eye(2) / np.sqrt(2.0)
