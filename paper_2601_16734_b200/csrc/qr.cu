@@ -1047,10 +1047,14 @@ __device__ __forceinline__ double re_of(cplx a) { return a.x; }
 // CTA of the cluster (DSMEM), one cluster barrier, then every warp forms the
 // same reflector (xLARFG convention) and updates its rows.  Partial slots are
 // double-buffered by column parity, so one barrier per column suffices.
-template <typename T, int RW, int NT>
+// RS > 0: each warp keeps RW of its rows in registers and RS more in (dynamic) shared memory
+// ([warp][row][lane], one element per lane): the 8192-row complex panels, whose 32 register
+// rows per lane would not fit in the 128-register budget of 512 threads.
+template <typename T, int RW, int NT, int RS = 0>
 __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int mp, int jb, T* Vall, int ldv, T* Tp) {
   constexpr bool CPX = Scalar<T>::is_complex;
   constexpr int NW = NT / 32;
+  constexpr int RT = RW + RS;  // rows per warp
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks(), b = (int)cl.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1059,13 +1063,23 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
   __shared__ T rowj[2][32];
   __shared__ T taus[QR_NB];
   __shared__ T S[QR_NB][QR_NB + 1];
-  const int g0 = (b * NW + warp) * RW;  // first row of this warp's slab
+  const int g0 = (b * NW + warp) * RT;  // first row of this warp's slab
   const bool colv = lane < jb;
   T a[RW];
+  extern __shared__ __align__(16) unsigned char qr_cl_dyn[];
+  T* srow = reinterpret_cast<T*>(qr_cl_dyn) + (size_t)warp * (RS > 0 ? RS : 1) * 32 + lane;
+  // row r of the slab: a register for r < RW, shared memory otherwise (r is a constant after unrolling)
+  auto getv = [&](int r) -> T { return r < RW ? a[r < RW ? r : 0] : srow[(r - RW) * 32]; };
+  auto setv = [&](int r, T v) {
+    if (r < RW)
+      a[r < RW ? r : 0] = v;
+    else
+      srow[(r - RW) * 32] = v;
+  };
 #pragma unroll
-  for (int r = 0; r < RW; ++r) {
+  for (int r = 0; r < RT; ++r) {
     const int g = g0 + r;
-    a[r] = (colv && g < mp) ? A[(size_t)g * lda + lane] : Scalar<T>::zero();
+    setv(r, (colv && g < mp) ? A[(size_t)g * lda + lane] : Scalar<T>::zero());
   }
   const int jr = jb < mp ? jb : mp;
   for (int j = 0; j < jr; ++j) {
@@ -1073,21 +1087,22 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
     // ---- partials
     T q = Scalar<T>::zero(), q2 = Scalar<T>::zero();
 #pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      const T x = shfl_t(a[r], j);
+    for (int r = 0; r < RT; ++r) {
+      const T ar = getv(r);
+      const T x = shfl_t(ar, j);
       const T y = (g0 + r > j) ? x : Scalar<T>::zero();
       if (r & 1)
-        q2 = fma_c(conj_(a[r]), y, q2);
+        q2 = fma_c(conj_(ar), y, q2);
       else
-        q = fma_c(conj_(a[r]), y, q);
+        q = fma_c(conj_(ar), y, q);
     }
     q = add(q, q2);
     // the owner of row j publishes it to every CTA
-    if (j >= g0 && j < g0 + RW) {
+    if (j >= g0 && j < g0 + RT) {
       T rv = Scalar<T>::zero();
 #pragma unroll
-      for (int r = 0; r < RW; ++r)
-        if (g0 + r == j) rv = a[r];
+      for (int r = 0; r < RT; ++r)
+        if (g0 + r == j) rv = getv(r);
       for (int g = 0; g < C; ++g) cl.map_shared_rank(&rowj[par][0], g)[lane] = rv;
     }
     wpart[warp][lane] = q;
@@ -1134,12 +1149,13 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
     if (tid == 0) taus[j] = tau;
     // ---- update: lane j stores v (rows > j) and beta; lanes c > j: a_c -= v f_c
 #pragma unroll
-    for (int r = 0; r < RW; ++r) {
+    for (int r = 0; r < RT; ++r) {
       const int g = g0 + r;
-      const T x = shfl_t(a[r], j);
+      const T ar = getv(r);
+      const T x = shfl_t(ar, j);
       const T v = (g > j) ? mul(x, sc) : (g == j ? Scalar<T>::one() : Scalar<T>::zero());
-      T nv = a[r];
-      if (lane > j) nv = sub(a[r], mul(v, f));
+      T nv = ar;
+      if (lane > j) nv = sub(ar, mul(v, f));
       if (lane == j) {
         if (g > j) nv = v;
         else if (g == j && refl) {
@@ -1149,17 +1165,18 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
             nv = beta;
         }
       }
-      a[r] = nv;
+      setv(r, nv);
     }
   }
   // ---- write back R (upper part) and V (unit lower trapezoid)
 #pragma unroll
-  for (int r = 0; r < RW; ++r) {
+  for (int r = 0; r < RT; ++r) {
     const int g = g0 + r;
     if (colv && g < mp) {
-      A[(size_t)g * lda + lane] = a[r];
+      const T ar = getv(r);
+      A[(size_t)g * lda + lane] = ar;
       Vall[(size_t)g * ldv + lane] =
-          (lane >= jr) ? Scalar<T>::zero() : (g > lane ? a[r] : (g == lane ? Scalar<T>::one() : Scalar<T>::zero()));
+          (lane >= jr) ? Scalar<T>::zero() : (g > lane ? ar : (g == lane ? Scalar<T>::one() : Scalar<T>::zero()));
     }
   }
   if (b == 0) {
@@ -1169,22 +1186,25 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
   cl.sync();  // no CTA leaves while peers may still write into its shared memory
 }
 
-template <typename T, int RW>
+template <typename T, int RW, int RS = 0>
 cudaError_t launch_panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* Tp, cudaStream_t s) {
   constexpr int NT = 512;
-  const int rows_cta = (NT / 32) * RW;
+  const int rows_cta = (NT / 32) * (RW + RS);
   const int C = (mp + rows_cta - 1) / rows_cta;
   if (C > 16) return cudaErrorInvalidValue;
+  const size_t dyn = (size_t)RS * NT * sizeof(T);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(qr_panel_cl_kernel<T, RW, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = cudaFuncSetAttribute(qr_panel_cl_kernel<T, RW, NT, RS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess && dyn > 0)
+      e = cudaFuncSetAttribute(qr_panel_cl_kernel<T, RW, NT, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1193,18 +1213,21 @@ cudaError_t launch_panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* T
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, qr_panel_cl_kernel<T, RW, NT>, Ap, lda, mp, jb, Vp, ldv, Tp);
+  return cudaLaunchKernelEx(&cfg, qr_panel_cl_kernel<T, RW, NT, RS>, Ap, lda, mp, jb, Vp, ldv, Tp);
 }
 
 // Rows per warp for an mp-row panel: the smallest slab that keeps the cluster
 // at <= 8 CTAs (<= 16 for the tallest panels); 0 = not eligible.
 template <typename T>
 cudaError_t panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* Tp, cudaStream_t s) {
-  constexpr int RWMAX = Scalar<T>::is_complex ? 16 : 32;
   if (mp <= 8 * 16 * 4) return launch_panel_cl<T, 4>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
   if (mp <= 8 * 16 * 8) return launch_panel_cl<T, 8>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
-  if (mp <= 16 * 16 * 16 || RWMAX == 16) return launch_panel_cl<T, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
-  return launch_panel_cl<T, RWMAX>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  if (mp <= 16 * 16 * 16) return launch_panel_cl<T, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  // 32 rows per warp: all in registers for real panels; complex: 16 in registers + 16 in shared memory
+  if constexpr (Scalar<T>::is_complex)
+    return launch_panel_cl<T, 16, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+  else
+    return launch_panel_cl<T, 32>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
 }
 
 bool panel_cl_enabled() {
@@ -1215,7 +1238,7 @@ bool panel_cl_enabled() {
   return on;
 }
 
-template <typename T> int panel_cl_max_rows() { return Scalar<T>::is_complex ? 16 * 16 * 16 : 16 * 16 * 32; }
+template <typename T> int panel_cl_max_rows() { return 16 * 16 * 32; }
 
 template <typename T>
 __global__ void conj_transpose_kernel(const T* src, long long s_src, int rows, int cols, T* dst, long long s_dst) {

@@ -56,7 +56,7 @@ def test_gemm_ops(dtype, opA, opB):
 @pytest.mark.parametrize("dtype", [np.float64, np.complex128])
 @pytest.mark.parametrize("shape", [(1, 1), (2, 3), (8, 4), (4, 8), (64, 32), (130, 70), (384, 192), (96, 200),
                                    (1000, 300), (257, 65), (4100, 70), (8192, 40), (2048, 300), (1100, 600),
-                                   (700, 700), (600, 1030)])
+                                   (700, 700), (600, 1030), (6000, 130)])
 def test_householder_qr(dtype, shape, blocked):
     lib = _lib()
     m, n = shape
