@@ -1224,10 +1224,15 @@ cudaError_t panel_cl(T* Ap, int lda, int mp, int jb, T* Vp, int ldv, T* Tp, cuda
   if (mp <= 8 * 16 * 8) return launch_panel_cl<T, 8>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
   if (mp <= 16 * 16 * 16) return launch_panel_cl<T, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
   // 32 rows per warp: all in registers for real panels; complex: 16 in registers + 16 in shared memory
+  static const int rs_real = [] {  // TTG_QR_RS=1: real panels split 16 + 16 as well
+    const char* e = getenv("TTG_QR_RS");
+    return e ? atoi(e) : 0;
+  }();
   if constexpr (Scalar<T>::is_complex)
     return launch_panel_cl<T, 16, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
   else
-    return launch_panel_cl<T, 32>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
+    return rs_real ? launch_panel_cl<T, 16, 16>(Ap, lda, mp, jb, Vp, ldv, Tp, s)
+                   : launch_panel_cl<T, 32>(Ap, lda, mp, jb, Vp, ldv, Tp, s);
 }
 
 bool panel_cl_enabled() {
