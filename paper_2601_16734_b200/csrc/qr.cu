@@ -1322,45 +1322,85 @@ size_t qr_blocked_elems(int m, int n, size_t* sA, size_t* sV, size_t* sT, size_t
 // triangular products read shared memory instead of L2.
 __host__ __device__ constexpr int tri_off(int r) { return r * QR_NBO - r * (r - 1) / 2; }
 
+// S[0:n0, n0:n0+w] and T_b are staged in shared memory before the products (they were read from L2
+// inside dependent loops), and the dot products run on four partial accumulators.
 template <typename T>
 __global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, const T* Tin, T* TO, int jbo,
                                                         long long stride) {
+  constexpr int ZS = QR_NB + 1;
+  constexpr int NTH = 256;
+  constexpr int MAXI = (QR_NBO - QR_NB) * QR_NB / NTH;  // items per thread of the largest block
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Z = reinterpret_cast<T*>(smem_raw);        // (QR_NBO - QR_NB) x (QR_NB + 1)
-  T* Tp = Z + (QR_NBO - QR_NB) * (QR_NB + 1);  // packed upper triangle of T_O
+  T* Z = reinterpret_cast<T*>(smem_raw);        // (QR_NBO - QR_NB) x ZS: S block, then Z
+  T* Tbs = Z + (QR_NBO - QR_NB) * ZS;           // QR_NB x ZS: T_b
+  T* Tp = Tbs + QR_NB * ZS;                     // packed upper triangle of T_O
   const int tid = threadIdx.x;
   S += stride * blockIdx.x;  // one CTA per chain
   Tin += stride * blockIdx.x;
   TO += stride * blockIdx.x;
   const int nbi = (jbo + QR_NB - 1) / QR_NB;
-  for (int r = tid / 32; r < QR_NBO; r += blockDim.x / 32)  // diagonal blocks T_b, zero elsewhere
+  for (int r = tid / 32; r < QR_NBO; r += NTH / 32)  // diagonal blocks T_b, zero elsewhere
     for (int c = r + (tid & 31); c < QR_NBO; c += 32) {
       const int br = r / QR_NB, bc = c / QR_NB;
       Tp[tri_off(r) + c - r] = (br == bc && r < jbo && c < jbo)
                                    ? Tin[(size_t)br * QR_NB * QR_NB + (r % QR_NB) * QR_NB + (c % QR_NB)]
                                    : Scalar<T>::zero();
     }
-  __syncthreads();
   for (int b = 1; b < nbi; ++b) {
     const int n0 = b * QR_NB, w = min(QR_NB, jbo - n0);
     const T* Tb = Tin + (size_t)b * QR_NB * QR_NB;
-    for (int idx = tid; idx < n0 * w; idx += blockDim.x) {  // Z = S[0:n0, n0:n0+w] T_b (T_b upper triangular)
+    __syncthreads();  // previous block's products are done with Z / T_b
+    for (int idx = tid; idx < n0 * w; idx += NTH) {
       const int r = idx / w, c = idx % w;
-      T z = Scalar<T>::zero();
-      for (int q = 0; q <= c; ++q) z = add(z, mul(S[(size_t)r * lds + n0 + q], Tb[q * QR_NB + c]));
-      Z[r * (QR_NB + 1) + c] = z;
+      Z[r * ZS + c] = S[(size_t)r * lds + n0 + c];
+    }
+    for (int idx = tid; idx < w * w; idx += NTH) {
+      const int r = idx / w, c = idx % w;
+      Tbs[r * ZS + c] = Tb[r * QR_NB + c];
     }
     __syncthreads();
-    for (int idx = tid; idx < n0 * w; idx += blockDim.x) {  // T_O[0:n0, n0:n0+w] = -T_O[0:n0, 0:n0] Z
+    T zr[MAXI];
+#pragma unroll
+    for (int it = 0; it < MAXI; ++it) {  // Z = S[0:n0, n0:n0+w] T_b (T_b upper triangular)
+      const int idx = tid + it * NTH;
+      zr[it] = Scalar<T>::zero();
+      if (idx < n0 * w) {
+        const int r = idx / w, c = idx % w;
+        const T* srow = Z + r * ZS;
+        T z0 = Scalar<T>::zero(), z1 = Scalar<T>::zero();
+        int q = 0;
+        for (; q + 1 <= c; q += 2) {
+          z0 = add(z0, mul(srow[q], Tbs[q * ZS + c]));
+          z1 = add(z1, mul(srow[q + 1], Tbs[(q + 1) * ZS + c]));
+        }
+        if (q <= c) z0 = add(z0, mul(srow[q], Tbs[q * ZS + c]));
+        zr[it] = add(z0, z1);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < MAXI; ++it) {
+      const int idx = tid + it * NTH;
+      if (idx < n0 * w) Z[(idx / w) * ZS + idx % w] = zr[it];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n0 * w; idx += NTH) {  // T_O[0:n0, n0:n0+w] = -T_O[0:n0, 0:n0] Z
       const int r = idx / w, c = idx % w;
       const T* row = Tp + tri_off(r) - r;  // row[q] = T_O[r][q], q >= r
-      T acc = Scalar<T>::zero();
-      for (int q = r; q < n0; ++q) acc = add(acc, mul(row[q], Z[q * (QR_NB + 1) + c]));
-      Tp[tri_off(r) + n0 + c - r] = sub(Scalar<T>::zero(), acc);
+      T a0 = Scalar<T>::zero(), a1 = Scalar<T>::zero(), a2 = Scalar<T>::zero(), a3 = Scalar<T>::zero();
+      int q = r;
+      for (; q + 3 < n0; q += 4) {
+        a0 = add(a0, mul(row[q], Z[q * ZS + c]));
+        a1 = add(a1, mul(row[q + 1], Z[(q + 1) * ZS + c]));
+        a2 = add(a2, mul(row[q + 2], Z[(q + 2) * ZS + c]));
+        a3 = add(a3, mul(row[q + 3], Z[(q + 3) * ZS + c]));
+      }
+      for (; q < n0; ++q) a0 = add(a0, mul(row[q], Z[q * ZS + c]));
+      Tp[tri_off(r) + n0 + c - r] = sub(Scalar<T>::zero(), add(add(a0, a1), add(a2, a3)));
     }
-    __syncthreads();
   }
-  for (int idx = tid; idx < QR_NBO * QR_NBO; idx += blockDim.x) {
+  __syncthreads();
+  for (int idx = tid; idx < QR_NBO * QR_NBO; idx += NTH) {
     const int r = idx / QR_NBO, c = idx % QR_NBO;
     TO[idx] = c >= r ? Tp[tri_off(r) + c - r] : Scalar<T>::zero();
   }
@@ -1368,7 +1408,7 @@ __global__ void __launch_bounds__(256) t_combine_kernel(const T* S, int lds, con
 
 template <typename T>
 constexpr size_t t_combine_smem() {
-  return ((size_t)(QR_NBO - QR_NB) * (QR_NB + 1) + (size_t)tri_off(QR_NBO)) * sizeof(T);
+  return ((size_t)(QR_NBO - QR_NB) * (QR_NB + 1) + (size_t)QR_NB * (QR_NB + 1) + (size_t)tri_off(QR_NBO)) * sizeof(T);
 }
 
 template <typename T>
