@@ -171,6 +171,12 @@ ttg_status ttg_mps_load(ttg_ctx* ctx, const char* path, int real_if_possible, tt
 ttg_status ttg_mps_save(ttg_ctx* ctx, const ttg_dmps* m, int chain, const char* path);
 ttg_status ttg_mpo_load(ttg_ctx* ctx, const char* path, int real_if_possible, ttg_dmpo** out);
 ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* op, const char* path);
+/* eigensolvers.hpp:15-64 detail::apply_effective_two_site(lenv, w1, w2, renv, x): y = H_eff x without
+ * forming H_eff.  dims = {D0, D1, D2, d1o, d1, d2o, d2, chiAo, chiA, chiBo, chiB} (w1: D0 x d1o x d1 x D1,
+ * w2: D1 x d2o x d2 x D2, Tensor4 row-major).  Host buffers, all of `dtype`: L[c0](a', a) as
+ * [D0][chiAo][chiA], R[c2](b', B) as [D2][chiBo][chiB], x[a][s1][s2][B], y[a'][s1'][s2'][b']. */
+ttg_status ttg_apply_effective_two_site(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
+                                        const void* W2, const void* R, const void* x, void* y);
 /* blas.hpp:128-138 expectation_mpo(op, u, v) = <u, op v> per chain (v NULL: v = u). */
 ttg_status ttg_expectation_mpo(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* u, const ttg_dmps* v, double* out_re,
                                double* out_im);

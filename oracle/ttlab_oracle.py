@@ -919,6 +919,53 @@ def update_left_op_environment(env, bra, op, ket):
     return np.einsum("cab,axy,cxsd,bsz->dyz", env, np.conj(bra), op, ket, optimize=True)
 
 
+def update_right_op_environment(env, bra, op, ket):
+    """environments.hpp:67-83: E'[c](a,b) = sum conj(A[a,s',a']) W[c,s',s,c'] E[c'](a',b') B[b,s,b'].
+    env has shape (c', a', b')."""
+    return np.einsum("dyz,axy,cxsd,bsz->cab", env, np.conj(bra), op, ket, optimize=True)
+
+
+def apply_effective_two_site(lenv, w1, w2, renv, x):
+    """eigensolvers.hpp:15-64 detail::apply_effective_two_site, step for step: X[c0] = L[c0] x
+    (:30-33), the W1 contraction into T[c1] (:34-46), the W2 contraction into U[c2] (:47-59), then
+    y = sum_c2 U[c2] R[c2]^T (:60-63).  lenv (D0, chiAo, chiA), renv (D2, chiBo, chiB)."""
+    L, R = np.asarray(lenv), np.asarray(renv)
+    w1, w2 = np.asarray(w1), np.asarray(w2)
+    chiAo, chiA = L.shape[1:]
+    chiBo, chiB = R.shape[1:]
+    D0, d1o, d1, D1 = w1.shape
+    _, d2o, d2, D2 = w2.shape
+    x = np.asarray(x).reshape(-1)
+    if x.size != chiA * d1 * d2 * chiB:
+        raise ShapeError("apply_effective_two_site: bad vector size")
+    xmat = x.reshape(chiA, d1 * d2 * chiB)
+    xl = [L[c0] @ xmat for c0 in range(D0)]
+    t = [np.zeros((chiAo * d1o, d2 * chiB), dtype=np.complex128) for _ in range(D1)]
+    for c0 in range(D0):
+        for s1o in range(d1o):
+            for s1 in range(d1):
+                for c1 in range(D1):
+                    w = w1[c0, s1o, s1, c1]
+                    if w == 0:
+                        continue
+                    for a in range(chiAo):
+                        t[c1][a * d1o + s1o] += w * xl[c0][a, s1 * d2 * chiB:(s1 + 1) * d2 * chiB]
+    u = [np.zeros((chiAo * d1o * d2o, chiB), dtype=np.complex128) for _ in range(D2)]
+    for c1 in range(D1):
+        for s2o in range(d2o):
+            for s2 in range(d2):
+                for c2 in range(D2):
+                    w = w2[c1, s2o, s2, c2]
+                    if w == 0:
+                        continue
+                    for row in range(chiAo * d1o):
+                        u[c2][row * d2o + s2o] += w * t[c1][row, s2 * chiB:(s2 + 1) * chiB]
+    y = np.zeros((chiAo * d1o * d2o, chiBo), dtype=np.complex128)
+    for c2 in range(D2):
+        y += u[c2] @ R[c2].T
+    return y.reshape(-1)
+
+
 def expectation_mpo(op: MPO, u: MPS, v: Optional[MPS] = None):
     """blas.hpp:128-138."""
     ket = v if v is not None else u

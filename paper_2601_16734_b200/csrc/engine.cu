@@ -1940,3 +1940,113 @@ ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* w, const char* path) {
 
 }  // extern "C"
 
+
+// ---------------------------------------------------------------------------
+// Two-site effective operator matvec (eigensolvers.hpp:15-64, apply_effective_two_site):
+//   y[a', s1', s2', b'] = sum L[c0](a', a) W1[c0, s1', s1, c1] W2[c1, s2', s2, c2] R[c2](b', B)
+//                         x[a, s1, s2, B]
+// B200 form: one DMMA GEMM for the left environment over all c0 at once (L stacked
+// (D0 chiAo) x chiA), one memory-bound kernel that contracts both MPO sites together
+// (the MPO entries live in shared memory, outputs written along B so loads and stores
+// coalesce), then D2 accumulating DMMA GEMMs against R[c2]^T.
+// ---------------------------------------------------------------------------
+namespace ttg {
+namespace {
+template <typename T>
+__global__ void heff_mix_kernel(const T* XL, const T* W1, const T* W2, T* V, int D0, int D1, int D2, int d1o, int d1,
+                                int d2o, int d2, int chiAo, int chiB) {
+  extern __shared__ __align__(16) unsigned char heff_smem[];
+  T* w1 = reinterpret_cast<T*>(heff_smem);
+  T* w2 = w1 + D0 * d1o * d1 * D1;
+  for (int i = threadIdx.x; i < D0 * d1o * d1 * D1; i += blockDim.x) w1[i] = W1[i];
+  for (int i = threadIdx.x; i < D1 * d2o * d2 * D2; i += blockDim.x) w2[i] = W2[i];
+  __syncthreads();
+  // V[a'][s1'][s2'][c2][B]; XL[c0][a'][s1][s2][B]
+  const long long total = (long long)chiAo * d1o * d2o * D2 * chiB;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    const int B = (int)(t % chiB);
+    t /= chiB;
+    const int c2 = (int)(t % D2);
+    t /= D2;
+    const int s2o = (int)(t % d2o);
+    t /= d2o;
+    const int s1o = (int)(t % d1o);
+    const int a = (int)(t / d1o);
+    T acc = Scalar<T>::zero();
+    for (int c0 = 0; c0 < D0; ++c0)
+      for (int s1 = 0; s1 < d1; ++s1)
+        for (int s2 = 0; s2 < d2; ++s2) {
+          T w = Scalar<T>::zero();
+          for (int c1 = 0; c1 < D1; ++c1)
+            w = add(w, mul(w1[((c0 * d1o + s1o) * d1 + s1) * D1 + c1], w2[((c1 * d2o + s2o) * d2 + s2) * D2 + c2]));
+          const T x = XL[((((size_t)c0 * chiAo + a) * d1 + s1) * d2 + s2) * chiB + B];
+          acc = add(acc, mul(w, x));
+        }
+    V[idx] = acc;
+  }
+}
+
+template <typename T>
+void heff_two_site(ttg_ctx* ctx, const int* dm, const void* hL, const void* hW1, const void* hW2, const void* hR,
+                   const void* hx, void* hy) {
+  const int D0 = dm[0], D1 = dm[1], D2 = dm[2], d1o = dm[3], d1 = dm[4], d2o = dm[5], d2 = dm[6];
+  const int chiAo = dm[7], chiA = dm[8], chiBo = dm[9], chiB = dm[10];
+  cudaStream_t st = ctx->stream;
+  const size_t es = sizeof(T);
+  const size_t nL = (size_t)D0 * chiAo * chiA, nW1 = (size_t)D0 * d1o * d1 * D1, nW2 = (size_t)D1 * d2o * d2 * D2;
+  const size_t nR = (size_t)D2 * chiBo * chiB, nx = (size_t)chiA * d1 * d2 * chiB;
+  const size_t nXL = (size_t)D0 * chiAo * d1 * d2 * chiB, nV = (size_t)chiAo * d1o * d2o * D2 * chiB;
+  const size_t ny = (size_t)chiAo * d1o * d2o * chiBo;
+  DevBuf L(nL * es, st), W1(nW1 * es, st), W2(nW2 * es, st), R(nR * es, st), X(nx * es, st), XL(nXL * es, st),
+      V(nV * es, st), Y(ny * es, st);
+  CK(cudaMemcpyAsync(L.p, hL, nL * es, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(W1.p, hW1, nW1 * es, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(W2.p, hW2, nW2 * es, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(R.p, hR, nR * es, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(X.p, hx, nx * es, cudaMemcpyHostToDevice, st));
+  // XL = [L[0]; ...; L[D0-1]] x  ((D0 chiAo) x chiA times chiA x (d1 d2 chiB))
+  const int M1 = D0 * chiAo, N1 = d1 * d2 * chiB;
+  GemmParams g1{L.p, X.p, XL.p, 0, 0, 0, dconst(M1), dconst(N1), dconst(chiA), nullptr, 0, nullptr, 1.0, 0};
+  CK(gemm<T>(g1, OP_N, OP_N, M1, N1, 1, st, chiA));
+  const size_t smem = (nW1 + nW2) * es;
+  if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
+  const long long tot = (long long)nV;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256));
+  heff_mix_kernel<T><<<blocks, 256, smem, st>>>(static_cast<const T*>(XL.p), static_cast<const T*>(W1.p),
+                                                 static_cast<const T*>(W2.p), static_cast<T*>(V.p), D0, D1, D2, d1o,
+                                                 d1, d2o, d2, chiAo, chiB);
+  CK(cudaGetLastError());
+  // y += V[:, c2, :] R[c2]^T for every c2  ((chiAo d1o d2o) x chiB times chiB x chiBo)
+  const int M3 = chiAo * d1o * d2o;
+  for (int c2 = 0; c2 < D2; ++c2) {
+    GemmParams g3{static_cast<const T*>(V.p) + (size_t)c2 * chiB, static_cast<const T*>(R.p) + (size_t)c2 * chiBo * chiB,
+                  Y.p, 0, 0, 0, dconst(M3), dconst(chiBo), dconst(chiB), nullptr, 0, nullptr, 1.0, c2 > 0 ? 1 : 0};
+    g3.lda = (long long)D2 * chiB;
+    g3.ldb = chiB;
+    g3.ldc = chiBo;
+    CK(gemm<T>(g3, OP_N, OP_T, M3, chiBo, 1, st, chiB));
+  }
+  ctx->launches += 2 + D2;
+  CK(cudaMemcpyAsync(hy, Y.p, ny * es, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+}  // namespace
+}  // namespace ttg
+
+ttg_status ttg_apply_effective_two_site(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
+                                        const void* W2, const void* R, const void* x, void* y) {
+  return guarded(ctx, [&] {
+    if (!dims || !L || !W1 || !W2 || !R || !x || !y) throw Error{TTG_INVALID, "null argument"};
+    for (int i = 0; i < 11; ++i)
+      if (dims[i] <= 0) throw Error{TTG_SHAPE, "apply_effective_two_site: bad dimension"};
+    CK(cudaSetDevice(ctx->device));
+    if (dtype == TTG_C128)
+      ttg::heff_two_site<ttg::cplx>(ctx, dims, L, W1, W2, R, x, y);
+    else if (dtype == TTG_F64)
+      ttg::heff_two_site<double>(ctx, dims, L, W1, W2, R, x, y);
+    else
+      throw Error{TTG_INVALID, "apply_effective_two_site: dtype"};
+  });
+}

@@ -576,6 +576,39 @@ def expectation_mpo(op, u, v=None) -> np.ndarray:
     return np.array(re[:]) + 1j * np.array(im[:])
 
 
+def apply_effective_two_site(lenv, w1, w2, renv, x, ctx: Optional[Context] = None) -> np.ndarray:
+    """eigensolvers.hpp:15-64 (detail::apply_effective_two_site): y = H_eff x for the two-site
+    effective operator, on the device (one DMMA GEMM for the left environment, one kernel for both
+    MPO sites, D2 DMMA GEMMs for the right environment).  lenv: D0 matrices L[c0] (chiAo x chiA) or an
+    array (D0, chiAo, chiA); w1 (D0, d1o, d1, D1); w2 (D1, d2o, d2, D2); renv: D2 matrices R[c2]
+    (chiBo x chiB); x of size chiA d1 d2 chiB ordered (a, s1, s2, B).  Returns y ordered
+    (a', s1', s2', b')."""
+    L = np.asarray(lenv)
+    R = np.asarray(renv)
+    w1 = np.asarray(w1)
+    w2 = np.asarray(w2)
+    x = np.asarray(x).reshape(-1)
+    if L.ndim != 3 or R.ndim != 3 or w1.ndim != 4 or w2.ndim != 4:
+        raise ShapeError("apply_effective_two_site: bad operand ranks")
+    D0, d1o, d1, D1 = w1.shape
+    D1b, d2o, d2, D2 = w2.shape
+    _, chiAo, chiA = L.shape
+    _, chiBo, chiB = R.shape
+    if L.shape[0] != D0 or R.shape[0] != D2 or D1b != D1:
+        raise ShapeError("apply_effective_two_site: bond mismatch")
+    if x.size != chiA * d1 * d2 * chiB:  # eigensolvers.hpp:22-23
+        raise ShapeError("apply_effective_two_site: bad vector size")
+    cplx = any(np.iscomplexobj(a) for a in (L, R, w1, w2, x))
+    dt = np.complex128 if cplx else np.float64
+    L, R, w1, w2, x = (np.ascontiguousarray(a, dtype=dt) for a in (L, R, w1, w2, x))
+    y = np.empty(chiAo * d1o * d2o * chiBo, dtype=dt)
+    dims = (C.c_int * 11)(D0, D1, D2, d1o, d1, d2o, d2, chiAo, chiA, chiBo, chiB)
+    ctx = ctx or context()
+    ctx.check(lib.ttg_apply_effective_two_site(ctx.handle, _lib.TTG_C128 if cplx else _lib.TTG_F64, dims,
+                                               *[C.c_void_p(a.ctypes.data) for a in (L, w1, w2, R, x, y)]))
+    return y
+
+
 def expectation_local(v, op, site: int, op2=None, site2: Optional[int] = None) -> np.ndarray:
     """blas.hpp:100-125: <v, O_site v> or the two-point <v, O_site O2_site2 v>
     (not normalised).  The local operators become a bond-1 MPO (identity on
