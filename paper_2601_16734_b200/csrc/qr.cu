@@ -1066,6 +1066,8 @@ __global__ void __launch_bounds__(NT, 1) qr_panel_cl_kernel(T* A, int lda, int m
   const int g0 = (b * NW + warp) * RT;  // first row of this warp's slab
   const bool colv = lane < jb;
   T a[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) a[r] = Scalar<T>::zero();  // (overwritten by the load below)
   extern __shared__ __align__(16) unsigned char qr_cl_dyn[];
   T* srow = reinterpret_cast<T*>(qr_cl_dyn) + (size_t)warp * (RS > 0 ? RS : 1) * 32 + lane;
   // row r of the slab: a register for r < RW, shared memory otherwise (r is a constant after unrolling)
