@@ -1,16 +1,23 @@
-"""Benchmark of the MPO·MPS apply + simplify hot path (BASELINE.json config 2).
+"""Benchmark of the MPO·MPS apply + simplify hot path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
 
-One step = one full `apply(MPO, MPS, Strategy)` call (blas.hpp:8-11):
-MPO expansion + exact QR pass + truncating R->L pass + variational sweeps,
-with the inputs already resident in HBM.  `e2e` repeats the step through the
-public host API (host tensors in, host tensors out: H2D + call + D2H).
-Multi-GPU (torchrun, one rank per GPU): every rank compresses its own
-independent chain (seed + rank), no data-path collective; the per-rank
-(sweeps, residual, norm) are all-gathered over NCCL at the end (weak scaling).
+Default workload: BASELINE.json config 4 (random D=8 MPO applied to an n=30,
+chi=512 MPS, simplified back to chi=512 over 2 sweeps), the largest
+apply+simplify config and the one the FP64 tensor-peak target is set on.
+One step = one full `apply(MPO, MPS, Strategy)` call (blas.hpp:8-11): MPO
+expansion + exact QR pass + truncating R->L pass + variational sweeps, with the
+inputs already resident in HBM.  `e2e` repeats the step through the public host
+API (host tensors in, host tensors out: H2D + call + D2H).
 
-`--impl reference` times the CPU restatement of the reference (oracle/, the
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU).  Single-chain configs do
+not shard (the sweep is sequential along sites), so every rank compresses its
+own independent chain (seed + 1000*rank, weak scaling).  `c5_scaling` adds the
+batched config 5 (1024 chains) sharded over the N ranks with one NCCL
+all-gather of per-chain (norm, error, sweeps) per batch.
+
+`--impl reference` times the CPU restatement of the reference (oracle/; the
 reference itself cannot be built here: it needs Eigen3) on the host cores.
 """
 from __future__ import annotations
@@ -38,10 +45,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--chains", type=int, default=None, help="batch configs: total chains (default: config)")
+    ap.add_argument("--no-c5", action="store_true", help="skip the c5_scaling measurement")
+    ap.add_argument("--ref-step-s", type=float, default=10.0, help="reference arm: CPU seconds sampled per step")
     return ap.parse_args()
 
 
@@ -136,37 +145,30 @@ def _target_bonds(cfg, mps, W):
     return [1] + [a.shape[2] for a in mps[0]]
 
 
-def cpu_step_estimate(cfg, mps, W, threads):
-    """Bounded CPU sample for the large configs (C3/C4): one middle two-site
-    step of the sweep in reference arithmetic (pair-first project_pair,
-    forms.hpp:13-32, then schmidt_split) on the real target tensors, timed and
-    extrapolated to 2(n-1) steps per sweep (the QR pass is not included)."""
+LARGE = ("C3", "C4")  # configs whose full CPU call takes minutes: timed through oracle.cpu_model
+
+
+def _output_bonds(cfg, t_bonds):
+    """Output bond profile of the call: min(chi_out, d^k, d^(n-k), exact-pass rank)."""
+    from paper_2601_16734_b200 import flops as F
+    q = F.qr_pass_bonds(t_bonds, [cfg.d] * cfg.n)
+    return [max(1, min(cfg.out_chi, cfg.d ** k, cfg.d ** (cfg.n - k), q[k])) for k in range(cfg.n + 1)]
+
+
+def cpu_call_model(cfg, mps, W, threads, sweeps):
+    """Unit model of one full call in reference arithmetic (oracle/cpu_model.py)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
-    import numpy as np
-    from oracle import ttlab_oracle as O
-    n = cfg.n // 2 - 1
-    if cfg.kind == "apply":
-        sites = []
-        for k in (n, n + 1):
-            w, a = W[k].astype(np.complex128), mps[0][k].astype(np.complex128)
-            c = np.einsum("cjid,aib->cajdb", w, a)
-            sites.append(c.reshape(w.shape[0] * a.shape[0], w.shape[1], w.shape[3] * a.shape[2]))
-    else:
-        sites = []
-        for k in (n, n + 1):
-            a, b = mps[0][k], mps[1][k]
-            c = np.einsum("asc,bsd->abscd", a, b)
-            sites.append(c.reshape(a.shape[0] * b.shape[0], a.shape[1], a.shape[2] * b.shape[2]))
-    p = cfg.out_chi
-    rng = np.random.default_rng(0)
-    L = rng.standard_normal((p, sites[0].shape[0])) + 1j * rng.standard_normal((p, sites[0].shape[0]))
-    R = rng.standard_normal((p, sites[1].shape[2])) + 1j * rng.standard_normal((p, sites[1].shape[2]))
-    t0 = time.perf_counter()
-    f = O.project_pair(L, sites[0], sites[1], R)
-    O.split_pair(f, 2, 2, O.Strategy(max_bond=p, tolerance=cfg.tolerance), O.LEFT_TO_RIGHT)
-    step = time.perf_counter() - t0
-    per_sweep = 2 * (cfg.n - 1) * step
-    return 1.0 / per_sweep, step
+    from oracle.cpu_model import CallModel
+    t_b = _target_bonds(cfg, mps, W)
+    return CallModel(t_b, _output_bonds(cfg, t_b), [cfg.d] * cfg.n, sweeps, seed=cfg.seed)
+
+
+def _model_sample(cfg, model, wall):
+    return (f"unit model of one full {cfg.name} call in reference arithmetic (complex128, pair-first "
+            f"project_pair, scprod <T,T>; oracle/cpu_model.py): {model.units_timed()} units timed "
+            f"({wall:.0f} s, random operands of the exact unit shapes), covering {100 * model.coverage():.0f}% "
+            f"of the call's estimated work directly; the {model.total_units()} units of the call are summed "
+            "(untimed groups extrapolated from their kind's measured rate) - partial")
 
 
 def cpu_reference(cfg, mps, W, steps, warmup, threads):
@@ -220,6 +222,26 @@ def run_reference(args):
         print(json.dumps(line), flush=True)
         return
     cfg, mps, W = workload(args.config, 0)
+    if cfg.name in LARGE:
+        model = cpu_call_model(cfg, mps, W, threads, cfg.max_sweeps)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            model.measure(args.ref_step_s)
+        wall = time.perf_counter() - t0
+        t_call = model.estimate()
+        val = cfg.max_sweeps / t_call
+        line = {
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "sweeps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "partial": True,
+            "config": {"workload": _workload_desc(cfg), "parallelism": "host threads"},
+            "full_call_s_estimate": t_call, "sweeps_per_call": cfg.max_sweeps,
+            "cpu_baseline": {"value": val, "unit": "sweeps/s", "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} steps of ~{args.ref_step_s:.0f} s: " + _model_sample(cfg, model, wall)},
+            "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     val, dt, sweeps = cpu_reference(cfg, mps, W, args.steps, min(args.warmup, 1), threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "sweeps/s", "n_gpus": args.gpus,
@@ -277,6 +299,64 @@ def _roofline(prof, cfg_name=None):
     }
 
 
+def _need_gpus(torch, world):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: needs {world} CUDA device(s) (one rank per GPU), "
+                         f"found {torch.cuda.device_count() if torch.cuda.is_available() else 0}; no CPU fallback")
+
+
+def c5_scaling(ttlab, torch, dist, ctx, stream, rank, world, steps=3):
+    """Config 5 (1024 chains, chi 128 -> 64) sharded over the ranks: chains/s at
+    this N and T1/(N T_N), T1 timed on rank 0 with the whole batch."""
+    from paper_2601_16734_b200.batch import gather_chain_stats
+    cfg, chains, _ = workload("C5", rank, world)
+    total = cfg.batch
+    strat = ttlab.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def timed(batch, nsteps, collective):
+        ttlab.simplify(batch, strat)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sweeps = 0
+        e0.record(stream)
+        for _ in range(nsteps):
+            reps = []
+            ttlab.simplify(batch, strat, report=reps)
+            st = torch.tensor([[r["norm"], r["error"], float(r["sweeps"])] for r in reps], dtype=torch.float64,
+                              device=dev)
+            allst = gather_chain_stats(st, total, world) if collective else st
+            sweeps += int(allst[:, 2].sum().item())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / nsteps, sweeps / nsteps
+
+    batch = ttlab.DeviceMPS.from_batch(chains, ctx=ctx)
+    if world > 1:
+        dist.barrier()
+    ms, sweeps = timed(batch, steps, True)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_n = float(t[0])
+    del batch
+    t_1 = t_n
+    if world > 1:
+        if rank == 0:
+            _, full, _ = workload("C5", 0, 1)
+            fb = ttlab.DeviceMPS.from_batch(full, ctx=ctx)
+            t_1, _ = timed(fb, steps, False)
+            del fb
+        t1 = torch.tensor([t_1], dtype=torch.float64, device=dev)
+        dist.broadcast(t1, 0)
+        t_1 = float(t1[0])
+    return {"workload": f"C5: {total} chains n={cfg.n} chi={cfg.chi}->{cfg.out_chi}, {total // world} per GPU, "
+                        "NCCL all-gather of per-chain (norm, error, sweeps) per batch",
+            "n_gpus": world, "ms_per_batch": t_n, "chains_per_s": total / (t_n / 1e3),
+            "sweeps_per_batch": sweeps, "t1_ms_per_batch": t_1, "efficiency_t1_over_n_tn": t_1 / (world * t_n),
+            "steps": steps}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -286,6 +366,7 @@ def run_ours(args):
     from paper_2601_16734_b200 import ttlab
 
     rank, world, local = dist_env()
+    _need_gpus(torch, world)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -383,15 +464,24 @@ def run_ours(args):
         ctx.profile_enable(False)
         roofline = _roofline(prof, cfg.name)
 
+    if roofline is not None:
+        roofline["call"] = {"F_alg_tflop": f_alg / 1e12, "achieved": tflops, "frac": tflops / FP64_DMMA_PEAK_TFLOPS,
+                            "note": "whole call: algorithmic flops (SURVEY §8d F_alg) / device time per call"}
+    c5 = None
+    if not args.no_c5:
+        c5 = c5_scaling(ttlab, torch, dist, ctx, stream, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        if cfg.name in ("C3", "C4"):
-            v, step = cpu_step_estimate(cfg, mps, W, threads)
-            cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port",
-                   "sample": f"one middle two-site step of {cfg.name} ({step:.1f} s: pair-first project_pair + "
-                             f"schmidt_split, complex128) extrapolated to {2 * (cfg.n - 1)} steps per sweep; "
-                             "QR pass excluded (partial)"}
+        if cfg.name in LARGE:
+            model = cpu_call_model(cfg, mps, W, threads, int(round(sweeps / args.steps)))
+            t0 = time.perf_counter()
+            model.measure(25.0)
+            wall = time.perf_counter() - t0
+            v = int(round(sweeps / args.steps)) / model.estimate()
+            cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port", "partial": True,
+                   "full_call_s_estimate": model.estimate(), "sample": _model_sample(cfg, model, wall)}
         else:
             v, dt, sw = cpu_reference(cfg, mps, W, 1, 0, threads)
             cpu = {"value": v, "unit": "sweeps/s", "cores": threads, "kind": "port",
@@ -415,6 +505,7 @@ def run_ours(args):
             "profile": prof,
             "cpu_baseline": cpu,
             "clocks": clk,
+            "c5_scaling": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -462,6 +553,7 @@ def run_ours_batch(args):
     from paper_2601_16734_b200.batch import gather_chain_stats
 
     rank, world, local = dist_env()
+    _need_gpus(torch, world)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -566,8 +658,27 @@ def run_ours_batch(args):
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: re-launch this script with N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     from paper_2601_16734_b200 import inputs as I
     batch = I.CONFIGS[args.config].kind == "batch"
     if args.impl == "reference":

@@ -29,6 +29,12 @@ DENSE_VECTOR_GUARD = 1 << 26  # mps.hpp:15
 DENSE_OPERATOR_GUARD = 1 << 13  # mpo.hpp:10
 
 SVD_TRUNCATE, VARIATIONAL = 0, 1  # types.hpp:39
+
+# Diagnostics: when a list, every truncating schmidt_split
+# appends (rows, cols, rank, s_r-1, s_r, relative gap (s_{r-1} - s_r) / s_{r-1})
+# for splits that drop singular values.  The gap decides how sensitive the kept
+# subspace is to rounding, i.e. whether 1e-10 parity is reachable.
+GAP_LOG: Optional[list] = None
 LEFT_TO_RIGHT, RIGHT_TO_LEFT = 0, 1  # types.hpp:41
 
 
@@ -370,6 +376,9 @@ def schmidt_split(theta: np.ndarray, strategy: Strategy, direction=LEFT_TO_RIGHT
     u, s, vh = svd_with_retry(theta)
     rank = truncation_rank(s, strategy)
     err = dropped_weight(s, rank)
+    if GAP_LOG is not None and rank < s.size and s[rank - 1] > 0:
+        GAP_LOG.append((theta.shape[0], theta.shape[1], rank, float(s[rank - 1]), float(s[rank]),
+                        float((s[rank - 1] - s[rank]) / s[rank - 1])))
     if direction == LEFT_TO_RIGHT:
         return u[:, :rank], s[:rank, None] * vh[:rank], err
     return u[:, :rank] * s[None, :rank], vh[:rank], err

@@ -68,6 +68,6 @@ struct ChainState {
   int status;           // 0 ok, else TTG_NUMERIC bit flags
 };
 
-enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2 };
+enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2, ST_RETRY = 4 };  // ST_RETRY: split pending a jitter retry
 
 }  // namespace ttg

@@ -84,7 +84,20 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   const char* ge = getenv("TTG_DEBUG_SVD_GRID");
   const bool use_grid = ge && ge[0] == '1' && jacobi_grid_eligible(l, k, 1, sizeof(T));
   Buf gw(use_grid ? jacobi_grid_work_bytes(l, k, sizeof(T)) : 16);
-  cudaError_t e = use_grid ? jacobi_svd_grid<T>(p, l, k, 1, gw.p, nullptr) : jacobi_svd<T>(p, l, k, 1, nullptr);
+  p.retry = 1;
+  {
+    const char* fr = getenv("TTG_SVD_FORCE_RETRY");
+    p.first_budget = fr ? atoi(fr) : 0;
+  }
+  cudaError_t e = cudaSuccess;
+  for (int attempt = 0; attempt < 2 && e == cudaSuccess; ++attempt) {
+    p.attempt = attempt;
+    if (attempt == 1) e = svd_jitter<T>(th.p, 0, p.M, p.N, p.bonds, p.ld, p.st, 1, nullptr);
+    if (e == cudaSuccess)
+      e = use_grid ? jacobi_svd_grid<T>(p, l, k, 1, gw.p, nullptr) : jacobi_svd<T>(p, l, k, 1, nullptr);
+  }
+  if (e == cudaSuccess && iso_complete_smem(l, kmin, sizeof(T)) <= 200 * 1024)
+    e = iso_complete<T>(p, l, kmin, 1, nullptr);
   cudaEventRecord(e1, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return TTG_CUDA;

@@ -226,6 +226,8 @@ struct Engine {
   int pre_slot = 0;
   int ld = 0;
   ChainState* d_state = nullptr;
+  double* svals = nullptr;  // sorted singular values of the last split (isometry completion)
+  long long svals_cap = 0;
 
   Engine(ttg_ctx* c, int L_, int B_) : ctx(c), st(c->stream), L(L_), B(B_) {}
 
@@ -353,18 +355,47 @@ struct Engine {
       CK(cudaMemsetAsync(ctx->d_sweeps, 0, B * sizeof(int), st));
       p.sweeps_out = B <= 4096 ? ctx->d_sweeps : nullptr;
     }
+    // kept numerically-zero singular values (sigma <= l eps |theta|_F <= l sqrt(k) eps sigma_0) are
+    // possible only when tol < l sqrt(k) eps: then the isometry is completed after the sweeps
+    const bool complete = svals && std::min(l, k) <= svals_cap && tol < (double)l * std::sqrt((double)k) * 2.3e-16 &&
+                          iso_complete_smem(l, std::min(l, k), sizeof(T)) <= 200 * 1024;
+    if (complete) {
+      p.svals = svals;
+      p.s_svals = svals_cap;
+    }
+    // retry policy (schmidt.hpp:23-35): a split that does not converge is jittered in place and
+    // relaunched once for the flagged chains (two launches that exit at once otherwise)
+    static const int force_retry = [] {
+      const char* e = getenv("TTG_SVD_FORCE_RETRY");  // test hook: sweeps allowed in the first attempt
+      return e ? atoi(e) : 0;
+    }();
+    p.retry = 1;
+    p.first_budget = force_retry;
     {
       ProfScope ps(ctx, TTG_PROF_SVD, flops);
       static const bool grid_ok = [] {
         const char* e = getenv("TTG_SVD_GRID");
         return !(e && e[0] == '0');
       }();
-      if (grid_ok && svd_grid_work && jacobi_grid_eligible(l, k, B, sizeof(T)))
-        CK(jacobi_svd_grid<T>(p, l, k, B, svd_grid_work, st));
-      else
-        CK(jacobi_svd<T>(p, l, k, B, st));
+      const bool grid = grid_ok && svd_grid_work && jacobi_grid_eligible(l, k, B, sizeof(T));
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        p.attempt = attempt;
+        if (attempt == 1) {
+          p.theta_pre = nullptr;
+          CK(svd_jitter<T>(const_cast<void*>(theta), s_theta, M, N, d_bonds, ld, d_state, B, st));
+          ++ctx->launches;
+        }
+        if (grid)
+          CK(jacobi_svd_grid<T>(p, l, k, B, svd_grid_work, st));
+        else
+          CK(jacobi_svd<T>(p, l, k, B, st));
+        ++ctx->launches;
+      }
+      if (complete) {
+        CK(iso_complete<T>(p, l, std::min(l, k), B, st));
+        ++ctx->launches;
+      }
     }
-    ++ctx->launches;
     if (ctx->profile && p.sweeps_out) {
       std::vector<int> hsw(B);
       CK(cudaMemcpyAsync(hsw.data(), ctx->d_sweeps, B * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -592,6 +623,9 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   E.svd_grid_work = B <= 16 ? svdg.p : nullptr;
   E.pre_cap = std::min(svd_lk, 256LL) * std::min(svd_lk, 256LL);  // small preconditioned splits only
   DevBuf prebuf((size_t)B * 4 * E.pre_cap * es, st);
+  DevBuf svbuf((size_t)B * svd_lk * sizeof(double), st);
+  E.svals = svbuf.as<double>();
+  E.svals_cap = svd_lk;
   E.pre_buf = prebuf.p;
   E.pre_slot = L + 2;
   const long long sC = P.ccap, sR = P.rcap, sBb = P.bcap;
@@ -1176,13 +1210,22 @@ ttg_status ttg_mps_from_device(ttg_ctx* ctx, int n, int dtype, int count, const 
                                const void* const* dev_sites, const double* errors, ttg_dmps** out) {
   return guarded(ctx, [&] {
     if (!bonds || !phys || !dev_sites || !out || count < 1 || n < 1) throw Error{TTG_INVALID, "bad argument"};
+    if (dtype != TTG_F64 && dtype != TTG_C128) throw Error{TTG_INVALID, "unknown dtype"};
     if (bonds[0] != 1 || bonds[n] != 1) throw Error{TTG_SHAPE, "MPS boundary bonds must have size one"};
     std::vector<int> ph(n);
     std::vector<long long> cap(n);
     for (int k = 0; k < n; ++k) {
+      if (bonds[k] < 1 || phys[k] < 1 || bonds[k + 1] < 1 || !dev_sites[k])
+        throw Error{TTG_SHAPE, "Tensor3 dimensions must be >= 1"};
       ph[k] = (int)phys[k];
       cap[k] = bonds[k] * phys[k] * bonds[k + 1];
     }
+    if (errors)
+      for (int c = 0; c < count; ++c)
+        if (!(errors[c] >= 0)) throw Error{TTG_SHAPE, "MPS error bound must be non-negative"};
+    // the source buffers belong to the caller (e.g. torch tensors on another stream): order the copy after
+    // all work already submitted to the device and finish it before returning (calls are synchronous)
+    CK(cudaDeviceSynchronize());
     ttg_dmps* m = new_dmps(n, dtype, count, ph, cap, ctx->stream);
     std::unique_ptr<ttg_dmps> guard(m);
     for (int c = 0; c < count; ++c) {
@@ -1192,6 +1235,7 @@ ttg_status ttg_mps_from_device(ttg_ctx* ctx, int n, int dtype, int count, const 
     for (int k = 0; k < n; ++k)
       CK(cudaMemcpyAsync(m->site[k], dev_sites[k], (size_t)count * cap[k] * esize(dtype), cudaMemcpyDeviceToDevice,
                          ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     *out = guard.release();
   });
 }
@@ -1589,6 +1633,8 @@ ttg_status ttg_scprod(ttg_ctx* ctx, const ttg_dmps* u, const ttg_dmps* v, double
     if (!u || !v || !out_re) throw Error{TTG_INVALID, "null argument"};
     if (u->n != v->n) throw Error{TTG_SHAPE, "scprod: states of different length"};  // mps.hpp:417-418
     if (u->count != v->count) throw Error{TTG_SHAPE, "scprod: batch sizes differ"};
+    for (int k = 0; k < u->n; ++k)
+      if (u->phys[k] != v->phys[k]) throw Error{TTG_SHAPE, "scprod: physical dimensions differ"};
     if (!u->uniform() || !v->uniform()) throw Error{TTG_SHAPE, "scprod on a batch needs identical shapes"};
     const int dtype = (u->dtype == TTG_C128 || v->dtype == TTG_C128) ? TTG_C128 : TTG_F64;
     std::unique_ptr<ttg_dmps> uc, vc;

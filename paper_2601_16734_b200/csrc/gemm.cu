@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
     }
   };
 
-  // split-K: blockIdx.z owns k-tiles [kt0, kt1); partial tiles are added atomically
+  // split-K: blockIdx.z owns k-tiles [kt0, kt1); its partial tile goes to the workspace
   const int ktiles_all = (K + BK - 1) / BK;
   const int splits = gridDim.z;
   const int per = (ktiles_all + splits - 1) / splits;
@@ -207,13 +207,12 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
         const int n = n0 + wn + j * 8 + 2 * t4 + (r & 1);
         if (m < M && n < N) {
           T* dst = C + m * ldc + n;
-          if (splits > 1) {  // C was zeroed (beta == 0) or holds the accumuland (beta == 1)
-            if constexpr (!CPX) {
-              atomicAdd(dst, alpha * acc[i][j][r]);
-            } else {
-              atomicAdd(&dst->x, alpha * acc[i][j][r]);
-              atomicAdd(&dst->y, alpha * acci[i][j][r]);
-            }
+          if (splits > 1) {  // partial tile of split z; reduced in order by splitk_reduce_kernel
+            T* w = static_cast<T*>(p.ws) + (((long long)chain * splits + blockIdx.z) * p.ws_m + m) * p.ws_n + n;
+            if constexpr (!CPX)
+              *w = alpha * acc[i][j][r];
+            else
+              *w = cplx{alpha * acc[i][j][r], alpha * acci[i][j][r]};
           } else if constexpr (!CPX) {
             const double v = alpha * acc[i][j][r];
             *dst = p.beta ? *dst + v : v;
@@ -226,18 +225,23 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       }
 }
 
+// Deterministic split-K: C (+)= sum over splits in split order.
 template <typename T>
-__global__ void zero_c_kernel(GemmParams p) {
+__global__ void splitk_reduce_kernel(GemmParams p, int splits) {
   const int chain = blockIdx.y;
   if (p.st && !p.st[chain].active) return;
   const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
   const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
   const long long ldc = p.ldc ? p.ldc : N;
   T* C = static_cast<T*>(p.C) + p.sC * chain;
+  const T* w = static_cast<const T*>(p.ws) + (long long)chain * splits * p.ws_m * p.ws_n;
+  const long long plane = (long long)p.ws_m * p.ws_n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)M * N;
        idx += (long long)gridDim.x * blockDim.x) {
     const long long m = idx / N, n = idx % N;
-    C[m * ldc + n] = Scalar<T>::zero();
+    T acc = p.beta ? C[m * ldc + n] : Scalar<T>::zero();
+    for (int z = 0; z < splits; ++z) acc = add(acc, w[z * plane + m * p.ws_n + n]);
+    C[m * ldc + n] = acc;
   }
 }
 
@@ -266,17 +270,30 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
     splits = (int)std::min<long long>((2 * 148 + tiles - 1) / tiles, kmax / 256);
     splits = std::max(1, std::min(splits, 64));
   }
-  if (splits > 1 && p.beta == 0) {
-    zero_c_kernel<T><<<dim3(std::max(1, std::min(148 * 4, (int)((long long)mmax * nmax / 256 + 1))), chains), 256, 0,
-                       s>>>(p);
-  }
   dim3 grid(tiles_m * tiles_n, chains, splits);
-  switch (opA) {
-    case OP_N: return launch_b<T, OP_N>(p, opB, grid, tiles_n, s);
-    case OP_T: return launch_b<T, OP_T>(p, opB, grid, tiles_n, s);
-    case OP_C: return launch_b<T, OP_C>(p, opB, grid, tiles_n, s);
-    default: return launch_b<T, OP_R>(p, opB, grid, tiles_n, s);
+  GemmParams q = p;
+  if (splits > 1) {  // partial tiles in a stream-ordered workspace, reduced in fixed order (deterministic)
+    q.ws_m = mmax;
+    q.ws_n = nmax;
+    cudaError_t e = cudaMallocAsync(&q.ws, (size_t)chains * splits * mmax * nmax * sizeof(T), s);
+    if (e != cudaSuccess) return e;
   }
+  cudaError_t e;
+  switch (opA) {
+    case OP_N: e = launch_b<T, OP_N>(q, opB, grid, tiles_n, s); break;
+    case OP_T: e = launch_b<T, OP_T>(q, opB, grid, tiles_n, s); break;
+    case OP_C: e = launch_b<T, OP_C>(q, opB, grid, tiles_n, s); break;
+    default: e = launch_b<T, OP_R>(q, opB, grid, tiles_n, s); break;
+  }
+  if (splits > 1) {
+    if (e == cudaSuccess) {
+      splitk_reduce_kernel<T><<<dim3(std::max(1, std::min(148 * 4, (int)((long long)mmax * nmax / 256 + 1))), chains),
+                                256, 0, s>>>(q, splits);
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(q.ws, s);
+  }
+  return e;
 }
 
 template cudaError_t gemm<double>(const GemmParams&, int, int, int, int, int, cudaStream_t, int);

@@ -26,6 +26,9 @@ struct GemmParams {
   int beta;  // 0: C = alpha*op(A)op(B); 1: C += alpha*op(A)op(B)
   // leading dimensions (row strides, elements) of the stored A, B, C; 0 = compact
   long long lda = 0, ldb = 0, ldc = 0;
+  // split-K partial tiles (set by gemm(): [chain][split][mmax][nmax], reduced in fixed order)
+  void* ws = nullptr;
+  int ws_m = 0, ws_n = 0;
 };
 
 // Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only);

@@ -43,6 +43,10 @@ struct SvdParams {
   int frame_ld;
   void* frame;        // full normalised frame (l x k row-major, columns sorted by singular value)
   long long s_frame;
+  // retry policy (schmidt.hpp:23-35, see svd_jitter)
+  int retry;          // 1: a non-converged first attempt flags ST_RETRY instead of ST_NOCONV
+  int attempt;        // 0: first attempt; 1: relaunch for the chains flagged ST_RETRY
+  int first_budget;   // > 0: sweep budget of the first attempt (forced-failure test hook)
 };
 
 // Shared-memory plan of the SVD kernel: per-column metadata plus, when it fits,
@@ -66,4 +70,23 @@ bool jacobi_grid_eligible(int lmax, int kmax, int chains, size_t es);
 template <typename T>
 cudaError_t jacobi_svd_grid(const SvdParams& p, int lmax, int kmax, int chains, void* work, cudaStream_t s);
 
+}  // namespace ttg
+
+namespace ttg {
+// Replace kept isometry vectors of numerically-zero singular values (sigma^2 <=
+// l^2 eps^2 |theta|_F^2) by orthonormal completions; needs p.svals (sorted,
+// min(m,n) per chain) from the preceding Jacobi launch.  lmax = isometry vector
+// length bound, kmax = rank bound.
+size_t iso_complete_smem(int lmax, int kmax, size_t es);
+template <typename T>
+cudaError_t iso_complete(const SvdParams& p, int lmax, int kmax, int chains, cudaStream_t s);
+}  // namespace ttg
+
+namespace ttg {
+// In-place jitter of theta for the chains flagged ST_RETRY: theta[i][j] +=
+// 1e-14 |theta|_F ((i + 31 j) % 7 / 7 + 1i ((3 i + j) % 5 / 5)) (schmidt.hpp:29-31;
+// real theta takes the real part).  Chains without the flag are untouched.
+template <typename T>
+cudaError_t svd_jitter(void* theta, long long s_theta, DimExpr M, DimExpr N, const int* bonds, int ld,
+                       const ChainState* st, int chains, cudaStream_t s);
 }  // namespace ttg

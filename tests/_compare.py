@@ -15,7 +15,7 @@ def rel(a, b):
 
 def spectra(tensors):
     """Per-bond Schmidt spectra from an exact canonical pass (metric 2)."""
-    c = O.canonicalize(O.MPS([t.astype(np.complex128) for t in tensors]), 0, O.NO_TRUNCATION)
+    c = O.canonicalize(O.MPS([np.asarray(t) for t in tensors]), 0, O.NO_TRUNCATION)
     out = []
     # move the centre right, recording the singular values of each cut
     psi = O.CanonicalMPS.raw([t.copy() for t in c.tensors], 0)
