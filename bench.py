@@ -121,7 +121,8 @@ def workload(cfg_name, rank, world=1, chains=None):
     if cfg.kind == "batch":
         total = chains or cfg.batch
         lo, hi = shard_range(total, world, rank)
-        return cfg, [I.config_inputs(cfg, chain=c)[0][0] for c in range(lo, hi)], None
+        workers = max(1, (os.cpu_count() or 1) // world)
+        return cfg, I.batch_inputs(cfg, lo, hi, workers), None
     import dataclasses
     cfg_r = dataclasses.replace(cfg, seed=cfg.seed + 1000 * rank)
     mps, W = I.config_inputs(cfg_r)

@@ -44,6 +44,7 @@ typedef enum {
 
 typedef enum { TTG_F64 = 0, TTG_C128 = 1 } ttg_dtype;
 typedef enum { TTG_SVD_TRUNCATE = 0, TTG_VARIATIONAL = 1 } ttg_truncation; /* types.hpp:39 */
+typedef enum { TTG_LEFT_TO_RIGHT = 0, TTG_RIGHT_TO_LEFT = 1 } ttg_direction; /* types.hpp:41 */
 
 /* types.hpp:50-88 Strategy.  max_bond <= 0 or >= INT32_MAX means unbounded. */
 typedef struct {
@@ -150,6 +151,21 @@ ttg_status ttg_apply(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* v, const 
 /* mps.hpp:310-313 canonicalize(MPS, centre, Strategy) (QR pass + truncating sweep). */
 ttg_status ttg_canonicalize(ttg_ctx* ctx, const ttg_dmps* v, int center, const ttg_strategy* strategy,
                             ttg_dmps** out, ttg_report* reports);
+/* CanonicalMPS::recenter (mps.hpp:268-279) on the device: `v` is a single chain canonical at
+ * `center`; the copy in *out is moved to `target` with the truncating moves move_center_right /
+ * move_center_left (mps.hpp:238-265) under `strategy`.  *err (may be NULL) = sqrt(sum of the squared
+ * dropped weights) of the moves; the error ledger of *out is NOT updated (the caller decides, as
+ * recenter and the single moves do differently).  Also canonicalize(const CanonicalMPS&)
+ * (mps.hpp:316-323). */
+ttg_status ttg_recenter(ttg_ctx* ctx, const ttg_dmps* v, int center, int target, const ttg_strategy* strategy,
+                        ttg_dmps** out, double* err);
+/* schmidt_split (schmidt.hpp:72-89) of one host m x n matrix (row-major, `dtype`) on the device:
+ * rank r = #{s_k > tolerance s_0} clamped to [1, max_bond]; LEFT_TO_RIGHT: a = U_r (m x r),
+ * b = S_r V_r^H (r x n); RIGHT_TO_LEFT: a = U_r S_r, b = V_r^H.  a needs m*min(m,n) and b
+ * min(m,n)*n elements of space; written compactly.  *err = sqrt(sum_{k>=r} s_k^2).  Used by
+ * CanonicalMPS::update_two_site / detail::split_pair (mps.hpp:164-173, 283-297). */
+ttg_status ttg_schmidt_split(ttg_ctx* ctx, int dtype, int64_t m, int64_t n, const void* theta, int direction,
+                             const ttg_strategy* strategy, void* a, void* b, int64_t* rank, double* err);
 /* mps.hpp:326-405 MPSSum(weights, states).join(): block-diagonal concatenation of the scaled
  * single-chain states (MPS::scaled semantics, mps.hpp:98-117); nterms = 1 gives states[0].scaled(w).
  * error = sum |w_l| err_l.  With the variational simplify this is combine / simplify(MPSSum)

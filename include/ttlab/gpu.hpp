@@ -218,6 +218,115 @@ inline CanonicalMPS::CanonicalMPS(const MPS& state, index_t center, const Strate
   *this = gpu::canonical_from(o.h, 0);
 }
 
+inline void CanonicalMPS::move_to(index_t target, const Strategy& strategy, double* err) {
+  *err = 0.0;
+  if (target == center_) return;
+  auto d = gpu::upload(*this);
+  const ttg_strategy s = gpu::to_c(strategy);
+  ttg_dmps* out = nullptr;
+  gpu::check(gpu::ctx(), ttg_recenter(gpu::ctx(), d.h, static_cast<int>(center_), static_cast<int>(target), &s, &out,
+                                      err));
+  gpu::DMps o(out);
+  double e = 0.0;
+  int c = 0;
+  tensors_ = gpu::download(o.h, 0, &e, &c);
+  center_ = target;
+}
+
+inline double CanonicalMPS::move_center_right(const Strategy& strategy) {  // mps.hpp:238-250
+  if (center_ + 1 >= size()) throw shape_error("move_center_right: already at the last site");
+  double e = 0.0;
+  move_to(center_ + 1, strategy, &e);
+  return e;
+}
+
+inline double CanonicalMPS::move_center_left(const Strategy& strategy) {  // mps.hpp:253-265
+  if (center_ == 0) throw shape_error("move_center_left: already at the first site");
+  double e = 0.0;
+  move_to(center_ - 1, strategy, &e);
+  return e;
+}
+
+inline CanonicalMPS& CanonicalMPS::recenter(index_t target, const Strategy& strategy) {  // mps.hpp:268-279
+  if (target < 0 || target >= size()) throw shape_error("recenter: center out of range");
+  double e = 0.0;
+  move_to(target, strategy, &e);
+  if (e > 0) update_error(e);
+  return *this;
+}
+
+namespace gpu {
+// Row-major host split through ttg_schmidt_split; a: m x r, b: r x n (row-major), returns r.
+inline index_t split_rowmajor(const std::vector<cplx>& theta, index_t m, index_t n, const Strategy& strategy,
+                              SweepDirection direction, std::vector<cplx>& a, std::vector<cplx>& b, double* err) {
+  const index_t k = std::min(m, n);
+  bool real = true;
+  for (const auto& x : theta) real = real && x.imag() == 0.0;
+  const ttg_strategy s = to_c(strategy);
+  const int dir = direction == SweepDirection::LEFT_TO_RIGHT ? TTG_LEFT_TO_RIGHT : TTG_RIGHT_TO_LEFT;
+  int64_t r = 0;
+  if (real) {
+    std::vector<double> th(theta.size()), ra(static_cast<size_t>(m * k)), rb(static_cast<size_t>(k * n));
+    for (size_t i = 0; i < th.size(); ++i) th[i] = theta[i].real();
+    check(ctx(), ttg_schmidt_split(ctx(), TTG_F64, m, n, th.data(), dir, &s, ra.data(), rb.data(), &r, err));
+    a.assign(ra.begin(), ra.begin() + m * r);
+    b.assign(rb.begin(), rb.begin() + r * n);
+  } else {
+    a.assign(static_cast<size_t>(m * k), cplx(0));
+    b.assign(static_cast<size_t>(k * n), cplx(0));
+    check(ctx(), ttg_schmidt_split(ctx(), TTG_C128, m, n, theta.data(), dir, &s, a.data(), b.data(), &r, err));
+    a.resize(static_cast<size_t>(m * r));
+    b.resize(static_cast<size_t>(r * n));
+  }
+  return r;
+}
+}  // namespace gpu
+
+inline SchmidtSplit schmidt_split(const Matrix& theta, const Strategy& strategy, SweepDirection direction) {
+  const index_t m = theta.rows(), n = theta.cols();
+  std::vector<cplx> th(static_cast<size_t>(m * n)), a, b;
+  for (index_t i = 0; i < m; ++i)
+    for (index_t j = 0; j < n; ++j) th[static_cast<size_t>(i * n + j)] = theta(i, j);
+  SchmidtSplit out;
+  const index_t r = gpu::split_rowmajor(th, m, n, strategy, direction, a, b, &out.error);
+  out.a = Matrix(m, r);
+  out.b = Matrix(r, n);
+  for (index_t i = 0; i < m; ++i)
+    for (index_t j = 0; j < r; ++j) out.a(i, j) = a[static_cast<size_t>(i * r + j)];
+  for (index_t i = 0; i < r; ++i)
+    for (index_t j = 0; j < n; ++j) out.b(i, j) = b[static_cast<size_t>(i * n + j)];
+  return out;
+}
+
+inline RealVector schmidt_values(const Matrix& theta) {
+  // b = S V^H of the untruncated split: the row norms are the singular values (descending)
+  const auto sp = schmidt_split(theta, NO_TRUNCATION, SweepDirection::LEFT_TO_RIGHT);
+  const index_t k = std::min(theta.rows(), theta.cols());
+  RealVector s(k);
+  for (index_t i = 0; i < k; ++i) {
+    double acc = 0.0;
+    if (i < sp.b.rows())
+      for (index_t j = 0; j < sp.b.cols(); ++j) acc += std::norm(sp.b(i, j));
+    s[i] = std::sqrt(acc);
+  }
+  return s;
+}
+
+namespace detail {
+inline PairSplit split_pair(const Tensor3& joined, index_t d1, index_t d2, const Strategy& strategy,
+                            SweepDirection direction) {  // mps.hpp:164-173
+  if (joined.phys_dim() != d1 * d2) throw shape_error("split_pair: fused physical dimension mismatch");
+  const index_t al = joined.left_dim(), ar = joined.right_dim();
+  std::vector<cplx> th(joined.data(), joined.data() + joined.size()), a, b;
+  double err = 0.0;
+  const index_t r = gpu::split_rowmajor(th, al * d1, d2 * ar, strategy, direction, a, b, &err);
+  PairSplit out{Tensor3(al, d1, r), Tensor3(r, d2, ar), err};
+  std::copy(a.begin(), a.end(), out.left.data());
+  std::copy(b.begin(), b.end(), out.right.data());
+  return out;
+}
+}  // namespace detail
+
 inline cplx scprod(const MPS& u, const MPS& v) {
   if (u.size() != v.size()) throw shape_error("scprod: states of different length");
   auto du = gpu::upload(u);

@@ -3,6 +3,8 @@
 // detail::apply_raw (:213-238, device).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "ttlab/mps.hpp"
@@ -29,6 +31,46 @@ public:
     std::vector<index_t> d{tensors_.empty() ? 1 : tensors_.front().left_dim()};
     for (const auto& t : tensors_) d.push_back(t.right_dim());
     return d;
+  }
+  std::vector<index_t> in_dimensions() const {  // mpo.hpp:42-47
+    std::vector<index_t> d;
+    for (const auto& t : tensors_) d.push_back(t.in_dim());
+    return d;
+  }
+  std::vector<index_t> out_dimensions() const {  // mpo.hpp:48-53
+    std::vector<index_t> d;
+    for (const auto& t : tensors_) d.push_back(t.out_dim());
+    return d;
+  }
+  /// mpo.hpp:54-74: |f|^(1/L) on every tensor, the phase on the first.
+  MPO scaled(cplx factor) const {
+    std::vector<Tensor4> out = tensors_;
+    const double mag = std::abs(factor);
+    if (mag == 0.0) {
+      for (auto& t : out) std::fill(t.data(), t.data() + t.size(), cplx(0));
+      return MPO(std::move(out));
+    }
+    const double root = std::pow(mag, 1.0 / static_cast<double>(size()));
+    const cplx phase = factor / mag;
+    for (size_t n = 0; n < out.size(); ++n) {
+      const cplx f = n == 0 ? root * phase : cplx(root);
+      for (index_t i = 0; i < out[n].size(); ++i) out[n].data()[i] *= f;
+    }
+    return MPO(std::move(out));
+  }
+  /// Hermitian adjoint: swap in/out indices and conjugate (mpo.hpp:77-92).
+  MPO adjoint() const {
+    std::vector<Tensor4> out;
+    out.reserve(tensors_.size());
+    for (const auto& t : tensors_) {
+      Tensor4 a(t.left_dim(), t.in_dim(), t.out_dim(), t.right_dim());
+      for (index_t c = 0; c < t.left_dim(); ++c)
+        for (index_t j = 0; j < t.out_dim(); ++j)
+          for (index_t i = 0; i < t.in_dim(); ++i)
+            for (index_t cp = 0; cp < t.right_dim(); ++cp) a(c, i, j, cp) = std::conj(t(c, j, i, cp));
+      out.push_back(std::move(a));
+    }
+    return MPO(std::move(out));
   }
 
 private:

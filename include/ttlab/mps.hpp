@@ -67,6 +67,13 @@ public:
     }
     return MPS(std::move(out), error_ * mag);
   }
+  /// mps.hpp:88-94
+  MPS conj() const {
+    std::vector<Tensor3> out;
+    out.reserve(tensors_.size());
+    for (const auto& t : tensors_) out.push_back(t.conj());
+    return MPS(std::move(out), error_);
+  }
   /// mps.hpp:120-126
   MPS zero_like() const {
     std::vector<Tensor3> out;
@@ -88,6 +95,43 @@ protected:
   double error_ = 0.0;
 };
 
+/// Truncated two-factor split theta ~= a b (schmidt.hpp:62-89), computed on the
+/// device (ttg_schmidt_split); LEFT_TO_RIGHT: a is an isometry, RIGHT_TO_LEFT: b is.
+struct SchmidtSplit {
+  Matrix a;  // rows x rank
+  Matrix b;  // rank x cols
+  double error;
+};
+SchmidtSplit schmidt_split(const Matrix& theta, const Strategy& strategy,
+                           SweepDirection direction = SweepDirection::LEFT_TO_RIGHT);
+/// Schmidt coefficients across a bipartition (schmidt.hpp:92-94), descending.
+RealVector schmidt_values(const Matrix& theta);
+
+namespace detail {
+/// Join neighbouring tensors into one with fused physical index (s1, s2) (mps.hpp:148-155).
+inline Tensor3 join_pair(const Tensor3& a, const Tensor3& b) {
+  if (a.right_dim() != b.left_dim()) throw shape_error("join_pair: bond mismatch");
+  Tensor3 out(a.left_dim(), a.phys_dim() * b.phys_dim(), b.right_dim());
+  const index_t rows = a.left_dim() * a.phys_dim(), inner = a.right_dim(), cols = b.phys_dim() * b.right_dim();
+  for (index_t i = 0; i < rows; ++i)
+    for (index_t k = 0; k < inner; ++k) {
+      const cplx x = a.data()[i * inner + k];
+      if (x == cplx(0)) continue;
+      for (index_t j = 0; j < cols; ++j) out.data()[i * cols + j] += x * b.data()[k * cols + j];
+    }
+  return out;
+}
+
+struct PairSplit {  // mps.hpp:157-161
+  Tensor3 left;
+  Tensor3 right;
+  double error;
+};
+/// Split a joined two-site tensor, truncating per `strategy` (mps.hpp:164-173, device).
+PairSplit split_pair(const Tensor3& joined, index_t d1, index_t d2, const Strategy& strategy,
+                     SweepDirection direction);
+}  // namespace detail
+
 /// MPS in canonical form around `center` (off-centre tensors are isometries).
 class CanonicalMPS : public MPS {
 public:
@@ -102,13 +146,56 @@ public:
     return n * n;
   }
   double norm() const { return tensors_[static_cast<size_t>(center_)].frobenius_norm(); }
+  /// mps.hpp:227-235
+  void normalize_in_place() {
+    const double n = norm();
+    if (n == 0.0) return;
+    auto& t = tensors_[static_cast<size_t>(center_)];
+    for (index_t i = 0; i < t.size(); ++i) t.data()[i] /= n;
+    error_ /= n;
+  }
+  /// Move the centre one site right / left, truncating per `strategy`; returns the
+  /// dropped weight (mps.hpp:238-265; device, ttg_recenter).
+  double move_center_right(const Strategy& strategy);
+  double move_center_left(const Strategy& strategy);
+  /// Recenter at `target`, accounting truncation in the error ledger (mps.hpp:268-279; device).
+  CanonicalMPS& recenter(index_t target, const Strategy& strategy);
+  /// Replace the (centre, neighbour) pair by the truncated split of `joined` and move the
+  /// centre in `direction` (mps.hpp:283-297; device split).
+  double update_two_site(const Tensor3& joined, SweepDirection direction, const Strategy& strategy) {
+    const index_t n = center_;
+    const bool to_right = direction == SweepDirection::LEFT_TO_RIGHT;
+    if ((to_right && n + 1 >= size()) || (!to_right && n == 0))
+      throw shape_error("update_two_site: no neighboring pair in that direction");
+    const index_t lo = to_right ? n : n - 1;
+    const index_t d1 = tensors_[static_cast<size_t>(lo)].phys_dim();
+    const index_t d2 = tensors_[static_cast<size_t>(lo + 1)].phys_dim();
+    auto split = detail::split_pair(joined, d1, d2, strategy, direction);
+    tensors_[static_cast<size_t>(lo)] = std::move(split.left);
+    tensors_[static_cast<size_t>(lo + 1)] = std::move(split.right);
+    center_ = to_right ? lo + 1 : lo;
+    return split.error;
+  }
+  /// Raw tensor write for sweep kernels; the caller maintains the isometry invariants (mps.hpp:301-302).
+  void set_tensor(index_t n, Tensor3 t) { tensors_[static_cast<size_t>(n)] = std::move(t); }
+  void set_center(index_t c) { center_ = c; }
 
 private:
+  void move_to(index_t target, const Strategy& strategy, double* err);  // device moves (gpu.hpp)
   index_t center_ = 0;
 };
 
 inline CanonicalMPS canonicalize(const MPS& state, index_t center = 0, const Strategy& strategy = DEFAULT_STRATEGY) {
   return CanonicalMPS(state, center, strategy);
+}
+
+/// Already-canonical input: just move the centre (mps.hpp:316-323).
+inline CanonicalMPS canonicalize(const CanonicalMPS& state, index_t center = 0,
+                                 const Strategy& strategy = DEFAULT_STRATEGY) {
+  CanonicalMPS out = state;
+  out.recenter(center, strategy);
+  if (strategy.normalize) out.normalize_in_place();
+  return out;
 }
 
 /// Lazy weighted sum of MPS with equal physical dimensions (mps.hpp:326-412).
@@ -143,7 +230,7 @@ inline double norm(const MPS& s) { return s.norm(); }
 inline double norm(const CanonicalMPS& s) { return s.norm(); }
 
 /// Dense vector (mps.hpp:438-449), most significant site first.
-inline std::vector<cplx> mps_to_dense(const MPS& state, index_t guard = DENSE_VECTOR_GUARD) {
+inline Vector mps_to_dense(const MPS& state, index_t guard = DENSE_VECTOR_GUARD) {
   const index_t dim = state.dimension(guard);
   std::vector<cplx> acc{cplx(1)};
   index_t rows = 1;
@@ -161,7 +248,11 @@ inline std::vector<cplx> mps_to_dense(const MPS& state, index_t guard = DENSE_VE
     acc = std::move(next);
   }
   if (rows != dim) throw shape_error("mps_to_dense: inconsistent contraction");
+#if TTLAB_HAS_EIGEN
+  return Eigen::Map<const Vector>(acc.data(), static_cast<index_t>(acc.size()));
+#else
   return acc;
+#endif
 }
 
 /// random_uniform_mps (mps.hpp:493-514): entries cplx(U(-1,1), U(-1,1)) from

@@ -71,6 +71,11 @@ SIGNATURES = {
                             C.POINTER(ttg_report)]),
     "ttg_canonicalize": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(ttg_strategy),
                                    C.POINTER(C.c_void_p), C.POINTER(ttg_report)]),
+    "ttg_recenter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(ttg_strategy),
+                               C.POINTER(C.c_void_p), C.POINTER(C.c_double)]),
+    "ttg_schmidt_split": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int,
+                                    C.POINTER(ttg_strategy), C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_double)]),
     "ttg_mps_join": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "ttg_simplify_sum": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),

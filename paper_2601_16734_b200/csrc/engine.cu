@@ -2096,3 +2096,191 @@ ttg_status ttg_apply_effective_two_site(ttg_ctx* ctx, int dtype, const int* dims
       throw Error{TTG_INVALID, "apply_effective_two_site: dtype"};
   });
 }
+
+// ---------------------------------------------------------------------------
+// CanonicalMPS centre moves and the truncated split on the device
+// (mps.hpp:238-297, schmidt.hpp:72-89)
+// ---------------------------------------------------------------------------
+namespace {
+
+// Split workspaces for an Engine that runs isolated splits of at most lmax x kmax.
+template <typename T>
+struct SplitWork {
+  DevBuf svdw, svdg, prebuf, svbuf;
+  long long svd_work = 0;
+  SplitWork(Engine<T>& E, long long lmax, long long kmax, int B, cudaStream_t st) {
+    const size_t es = sizeof(T);
+    const long long lk = std::max({lmax, kmax, 1LL});
+    svd_work = (lk + 1) * (lk + 1);  // any panel orientation outside shared memory
+    svdw = DevBuf((size_t)B * svd_work * es, st);
+    svdg = DevBuf(B <= 16 ? (size_t)B * jacobi_grid_work_bytes((int)lk, (int)lk, es) : 0, st);
+    E.svd_grid_work = B <= 16 ? svdg.p : nullptr;
+    E.pre_cap = std::min(lk, 256LL) * std::min(lk, 256LL);
+    prebuf = DevBuf((size_t)B * 4 * E.pre_cap * es, st);
+    E.pre_buf = prebuf.p;
+    E.pre_slot = E.ld - 1;
+    svbuf = DevBuf((size_t)B * lk * sizeof(double), st);
+    E.svals = svbuf.as<double>();
+    E.svals_cap = lk;
+  }
+};
+
+template <typename T>
+int read_bond(Engine<T>& E, int idx) {
+  int r = 0;
+  CK(cudaMemcpyAsync(&r, E.d_bonds + idx, sizeof(int), cudaMemcpyDeviceToHost, E.st));
+  CK(cudaStreamSynchronize(E.st));
+  return r;
+}
+
+// Move the centre of a canonical single chain from `center` to `target`,
+// truncating per strategy (recenter, mps.hpp:268-279, built from
+// move_center_right / move_center_left, mps.hpp:238-265).  Returns the
+// moved copy and sqrt(sum of the squared dropped weights).
+template <typename T>
+ttg_dmps* run_recenter(ttg_ctx* ctx, const ttg_dmps& in, int center, int target, const ttg_strategy& s, double* err) {
+  const int L = in.n;
+  cudaStream_t st = ctx->stream;
+  const size_t es = sizeof(T);
+  ttg_dmps* o = new_dmps(L, in.dtype, 1, in.phys, in.cap, st);
+  std::unique_ptr<ttg_dmps> guard(o);
+  o->bonds.assign(in.bonds.begin(), in.bonds.begin() + (L + 1));
+  o->error[0] = in.error[0];
+  for (int k = 0; k < L; ++k)
+    CK(cudaMemcpyAsync(o->site[k], in.site[k], (size_t)in.cap[k] * es, cudaMemcpyDeviceToDevice, st));
+  std::vector<int> b(o->bonds.begin(), o->bonds.end());
+  Engine<T> E(ctx, L, 1);
+  E.ld = L + 3;
+  long long lmax = 1, cmax = 1;
+  for (int k = 0; k < L; ++k) {
+    lmax = std::max({lmax, (long long)b[k] * in.phys[k], (long long)in.phys[k] * b[k + 1]});
+    cmax = std::max(cmax, in.cap[k]);
+  }
+  E.bound.assign(E.ld, (int)lmax);
+  DevBuf bonds_buf((size_t)E.ld * sizeof(int), st), state_buf(sizeof(ChainState), st);
+  E.d_bonds = bonds_buf.as<int>();
+  E.d_state = state_buf.as<ChainState>();
+  {
+    std::vector<int> hb(E.ld, 1);
+    for (int k = 0; k <= L; ++k) hb[k] = b[k];
+    CK(cudaMemcpyAsync(E.d_bonds, hb.data(), hb.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(init_state(E.d_state, 1, st));
+  SplitWork<T> work(E, lmax, lmax, 1, st);
+  DevBuf Th((size_t)cmax * es, st), Bb((size_t)lmax * lmax * es, st), X((size_t)cmax * es, st);
+  const int mb = clamp_bond(s.max_bond);
+  const double tol = s.tolerance;
+  int c = center;
+  while (c < target) {  // move_center_right (mps.hpp:238-250): theta = left unfolding of site c
+    const int m = b[c] * o->phys[c], n = b[c + 1];
+    CK(cudaMemcpyAsync(Th.p, o->site[c], (size_t)m * n * es, cudaMemcpyDeviceToDevice, st));
+    E.S(Th.p, 0, dconst(m), dconst(n), c + 1, o->site[c], 0, 0, tol, mb, false, true, work.svdw.p, work.svd_work);
+    const int r = read_bond(E, c + 1);
+    // S V^H = U_r^H theta (r x n), carried into site c+1 (mps.hpp:246)
+    E.G(o->site[c], 0, Th.p, 0, Bb.p, 0, dconst(r), dconst(n), dconst(m), OP_C, OP_N, false);
+    const int w = o->phys[c + 1] * b[c + 2];
+    E.G(Bb.p, 0, o->site[c + 1], 0, X.p, 0, dconst(r), dconst(w), dconst(n), OP_N, OP_N, false);
+    CK(cudaMemcpyAsync(o->site[c + 1], X.p, (size_t)r * w * es, cudaMemcpyDeviceToDevice, st));
+    b[c + 1] = r;
+    ++c;
+  }
+  while (c > target) {  // move_center_left (mps.hpp:253-265): theta = right unfolding of site c
+    const int m = b[c], n = o->phys[c] * b[c + 1];
+    CK(cudaMemcpyAsync(Th.p, o->site[c], (size_t)m * n * es, cudaMemcpyDeviceToDevice, st));
+    E.S(Th.p, 0, dconst(m), dconst(n), c, o->site[c], 0, 1, tol, mb, false, true, work.svdw.p, work.svd_work);
+    const int r = read_bond(E, c);
+    // U S = theta V_r (m x r), carried into site c-1 (mps.hpp:261)
+    E.G(Th.p, 0, o->site[c], 0, Bb.p, 0, dconst(m), dconst(r), dconst(n), OP_N, OP_C, false);
+    const int h = b[c - 1] * o->phys[c - 1];
+    E.G(o->site[c - 1], 0, Bb.p, 0, X.p, 0, dconst(h), dconst(r), dconst(m), OP_N, OP_N, false);
+    CK(cudaMemcpyAsync(o->site[c - 1], X.p, (size_t)h * r * es, cudaMemcpyDeviceToDevice, st));
+    b[c] = r;
+    --c;
+  }
+  ChainState hs{};
+  CK(cudaMemcpyAsync(&hs, E.d_state, sizeof hs, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hs.status & ST_NONFINITE) throw Error{TTG_NUMERIC, "schmidt_split: non-finite input"};
+  if (hs.status & ST_NOCONV) throw Error{TTG_NUMERIC, "SVD failed to converge"};
+  for (int k = 0; k <= L; ++k) o->bonds[k] = b[k];
+  o->center = target;
+  if (err) *err = std::sqrt(std::max(0.0, hs.err2));
+  return guard.release();
+}
+
+// schmidt_split (schmidt.hpp:72-89) of one host matrix on the device.
+template <typename T>
+void run_schmidt_split(ttg_ctx* ctx, int m, int n, const void* theta, int direction, const ttg_strategy& s, void* a,
+                       void* bout, int64_t* rank, double* err) {
+  cudaStream_t st = ctx->stream;
+  const size_t es = sizeof(T);
+  const int kmin = std::min(m, n);
+  Engine<T> E(ctx, 1, 1);
+  E.ld = 4;
+  E.bound.assign(E.ld, std::max(m, n));
+  DevBuf bonds_buf((size_t)E.ld * sizeof(int), st), state_buf(sizeof(ChainState), st);
+  E.d_bonds = bonds_buf.as<int>();
+  E.d_state = state_buf.as<ChainState>();
+  CK(cudaMemsetAsync(E.d_bonds, 0, E.ld * sizeof(int), st));
+  CK(init_state(E.d_state, 1, st));
+  SplitWork<T> work(E, std::max(m, n), std::max(m, n), 1, st);
+  DevBuf th((size_t)m * n * es, st), iso((size_t)std::max(m, n) * kmin * es, st), other((size_t)std::max(m, n) * kmin * es, st);
+  CK(cudaMemcpyAsync(th.p, theta, (size_t)m * n * es, cudaMemcpyHostToDevice, st));
+  const int mode = direction == TTG_RIGHT_TO_LEFT ? 1 : 0;
+  E.S(th.p, 0, dconst(m), dconst(n), 0, iso.p, 0, mode, s.tolerance, clamp_bond(s.max_bond), false, true,
+      work.svdw.p, work.svd_work);
+  const int r = read_bond(E, 0);
+  if (mode == 0) {  // a = U_r (m x r), b = S V^H = U_r^H theta (r x n)
+    E.G(iso.p, 0, th.p, 0, other.p, 0, dconst(r), dconst(n), dconst(m), OP_C, OP_N, false);
+    CK(cudaMemcpyAsync(a, iso.p, (size_t)m * r * es, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(bout, other.p, (size_t)r * n * es, cudaMemcpyDeviceToHost, st));
+  } else {  // b = V_r^H (r x n), a = U S = theta V_r (m x r)
+    E.G(th.p, 0, iso.p, 0, other.p, 0, dconst(m), dconst(r), dconst(n), OP_N, OP_C, false);
+    CK(cudaMemcpyAsync(a, other.p, (size_t)m * r * es, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(bout, iso.p, (size_t)r * n * es, cudaMemcpyDeviceToHost, st));
+  }
+  ChainState hs{};
+  CK(cudaMemcpyAsync(&hs, E.d_state, sizeof hs, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hs.status & ST_NONFINITE) throw Error{TTG_NUMERIC, "schmidt_split: non-finite input"};
+  if (hs.status & ST_NOCONV) throw Error{TTG_NUMERIC, "SVD failed to converge"};
+  *rank = r;
+  if (err) *err = std::sqrt(std::max(0.0, hs.err2));
+}
+
+}  // namespace
+
+extern "C" {
+
+ttg_status ttg_recenter(ttg_ctx* ctx, const ttg_dmps* v, int center, int target, const ttg_strategy* strategy,
+                        ttg_dmps** out, double* err) {
+  return guarded(ctx, [&] {
+    check_strategy(strategy);
+    if (!v || !out) throw Error{TTG_INVALID, "null argument"};
+    if (v->count != 1) throw Error{TTG_SHAPE, "recenter: single chains only"};
+    if (center < 0 || center >= v->n) throw Error{TTG_SHAPE, "recenter: center out of range"};
+    if (target < 0 || target >= v->n) throw Error{TTG_SHAPE, "recenter: center out of range"};  // mps.hpp:269-270
+    if (v->dtype == TTG_F64)
+      *out = run_recenter<double>(ctx, *v, center, target, *strategy, err);
+    else
+      *out = run_recenter<cplx>(ctx, *v, center, target, *strategy, err);
+  });
+}
+
+ttg_status ttg_schmidt_split(ttg_ctx* ctx, int dtype, int64_t m, int64_t n, const void* theta, int direction,
+                             const ttg_strategy* strategy, void* a, void* b, int64_t* rank, double* err) {
+  return guarded(ctx, [&] {
+    check_strategy(strategy);
+    if (!theta || !a || !b || !rank) throw Error{TTG_INVALID, "null argument"};
+    if (m < 1 || n < 1 || m > (1 << 30) / std::max<int64_t>(n, 1)) throw Error{TTG_SHAPE, "schmidt_split: bad shape"};
+    if (dtype == TTG_F64)
+      run_schmidt_split<double>(ctx, (int)m, (int)n, theta, direction, *strategy, a, b, rank, err);
+    else if (dtype == TTG_C128)
+      run_schmidt_split<cplx>(ctx, (int)m, (int)n, theta, direction, *strategy, a, b, rank, err);
+    else
+      throw Error{TTG_INVALID, "unknown dtype"};
+  });
+}
+
+}  // extern "C"

@@ -166,3 +166,31 @@ def config_inputs(cfg: Config, chain: int = 0) -> Tuple[list, list]:
         b = random_mps(cfg.n, cfg.d, cfg.chi, cfg.seed + 1, complex_=True)
         return [a, b], None
     raise ValueError(cfg.kind)
+
+
+def _batch_chain(args):
+    name, chain = args
+    return config_inputs(CONFIGS[name], chain=chain)[0][0]
+
+
+def batch_inputs(cfg: Config, lo: int, hi: int, workers: int = 0) -> list:
+    """Chains [lo, hi) of a batched config, generated on a pool of host processes
+    (the counter-based generator makes every chain independent of the others)."""
+    import multiprocessing as mp
+    import os
+    idx = list(range(lo, hi))
+    workers = workers or min(len(idx), os.cpu_count() or 1)
+    if workers <= 1 or len(idx) < 8:
+        return [config_inputs(cfg, chain=c)[0][0] for c in idx]
+    saved = {k: os.environ.get(k) for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in saved:
+        os.environ[k] = "1"  # single-threaded BLAS in the workers (inherited by the spawned processes)
+    try:
+        with mp.get_context("spawn").Pool(workers) as pool:
+            return pool.map(_batch_chain, [(cfg.name, c) for c in idx], chunksize=max(1, len(idx) // (4 * workers)))
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v

@@ -527,6 +527,40 @@ def canonicalize(v, center: int = 0, strategy: Strategy = DEFAULT_STRATEGY,
     return DeviceMPS(h, v.ctx)
 
 
+def recenter(v, target: int, strategy: Strategy = DEFAULT_STRATEGY, center: Optional[int] = None):
+    """CanonicalMPS::recenter / move_center_right / move_center_left (mps.hpp:238-279) on the
+    device: returns (moved state, err) with err = sqrt(sum of the squared dropped weights).  The
+    moved state keeps the input's error ledger (recenter adds err to it, the single moves do not:
+    the caller decides).  `center` defaults to the state's own centre (single chains)."""
+    v = _as_mps(v)
+    c = v.center if center is None else int(center)
+    if c < 0:
+        raise ShapeError("recenter: state is not in canonical form (give its centre)")
+    h, err = C.c_void_p(), C.c_double()
+    v.ctx.check(lib.ttg_recenter(v.ctx.handle, v.handle, c, int(target), C.byref(strategy._c()), C.byref(h),
+                                 C.byref(err)))
+    return DeviceMPS(h, v.ctx), err.value
+
+
+def schmidt_split(theta, strategy: Strategy, direction: int = 0, ctx: Optional[Context] = None):
+    """schmidt_split (schmidt.hpp:72-89) on the device: returns (a, b, error); direction 0 =
+    LEFT_TO_RIGHT (a isometric), 1 = RIGHT_TO_LEFT (b isometric)."""
+    ctx = ctx or context()
+    th = np.ascontiguousarray(theta)
+    cplx = np.iscomplexobj(th)
+    th = th.astype(np.complex128 if cplx else np.float64)
+    m, n = th.shape
+    k = min(m, n)
+    a = np.empty(m * k, dtype=th.dtype)
+    b = np.empty(k * n, dtype=th.dtype)
+    r, err = C.c_int64(), C.c_double()
+    ctx.check(lib.ttg_schmidt_split(ctx.handle, _lib.TTG_C128 if cplx else _lib.TTG_F64, m, n,
+                                    C.c_void_p(th.ctypes.data), int(direction), C.byref(strategy._c()),
+                                    C.c_void_p(a.ctypes.data), C.c_void_p(b.ctypes.data), C.byref(r), C.byref(err)))
+    r = r.value
+    return a[:m * r].reshape(m, r), b[:r * n].reshape(r, n), err.value
+
+
 def scprod(u, v) -> np.ndarray:
     """mps.hpp:416-423, one value per chain."""
     u = _as_mps(u)

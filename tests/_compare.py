@@ -30,9 +30,10 @@ def spectra(tensors):
 def distance(a, b):
     """|a - b| computed cancellation-free: join [a, -b] + exact canonicalization."""
     L = len(a)
+    dt = np.result_type(a[0], b[0])
     ts = []
     for n in range(L):
-        x, y = a[n].astype(np.complex128), -b[n].astype(np.complex128) if n == 0 else b[n].astype(np.complex128)
+        x, y = a[n].astype(dt), -b[n].astype(dt) if n == 0 else b[n].astype(dt)
         if L == 1:
             ts.append(x + y)
         elif n == 0:
@@ -40,7 +41,7 @@ def distance(a, b):
         elif n == L - 1:
             ts.append(np.concatenate([x, y], axis=0))
         else:
-            t = np.zeros((x.shape[0] + y.shape[0], x.shape[1], x.shape[2] + y.shape[2]), dtype=np.complex128)
+            t = np.zeros((x.shape[0] + y.shape[0], x.shape[1], x.shape[2] + y.shape[2]), dtype=dt)
             t[:x.shape[0], :, :x.shape[2]] = x
             t[x.shape[0]:, :, x.shape[2]:] = y
             ts.append(t)

@@ -264,6 +264,191 @@ int main() {
                         sizeof(cplx) * static_cast<size_t>(state[n].size())) == 0);
     std::remove(path.c_str());
   });
+  section("schmidt_split KATs on the device (test_core.cpp:73-101)", [] {
+    Matrix theta = Matrix::Identity(2, 2);
+    theta(0, 0) = theta(1, 1) = 1.0 / std::sqrt(2.0);
+    auto split = schmidt_split(theta, NO_TRUNCATION);
+    CHECK(split.error == 0.0);
+    CHECK((split.a * split.b - theta).norm() < 1e-14);
+    auto sv = schmidt_values(theta);
+    CHECK(std::abs(sv[0] - 1 / std::sqrt(2.0)) < 1e-15 && std::abs(sv[1] - 1 / std::sqrt(2.0)) < 1e-15);
+    auto s1 = schmidt_split(theta, NO_TRUNCATION.with_max_bond(1));
+    CHECK(std::abs(s1.error - 1 / std::sqrt(2.0)) < 1e-15);
+    CHECK(s1.a.cols() == 1);
+    Matrix r(4, 4);
+    MPS rs = random_uniform_mps(2, 4, 4, 5);  // 4 x 4 complex entries from the reference generator
+    for (index_t i = 0; i < 4; ++i)
+      for (index_t j = 0; j < 4; ++j) r(i, j) = rs[0](0, i, j) + rs[1](j, 0, 0) * 0.5;
+    auto s2 = schmidt_split(r, NO_TRUNCATION.with_max_bond(2));
+    CHECK(std::abs((s2.a * s2.b - r).norm() - s2.error) < 1e-12);
+    Matrix t6(6, 4);
+    MPS r6 = random_uniform_mps(2, 6, 4, 9);
+    for (index_t i = 0; i < 6; ++i)
+      for (index_t j = 0; j < 4; ++j) t6(i, j) = r6[0](0, i, j);
+    auto lr = schmidt_split(t6, NO_TRUNCATION, SweepDirection::LEFT_TO_RIGHT);
+    CHECK((lr.a.adjoint() * lr.a - Matrix::Identity(4, 4)).norm() < 1e-12);
+    auto rl = schmidt_split(t6, NO_TRUNCATION, SweepDirection::RIGHT_TO_LEFT);
+    CHECK((rl.b * rl.b.adjoint() - Matrix::Identity(4, 4)).norm() < 1e-12);
+    CHECK((rl.a * rl.b - t6).norm() < 1e-12);
+  });
+  auto isometries_ok = [](const CanonicalMPS& st) {
+    for (index_t n = 0; n < st.size(); ++n) {
+      const Tensor3& t = st[n];
+      if (n < st.center()) {  // left unfolding a^H a = I
+        const index_t rows = t.left_dim() * t.phys_dim(), c = t.right_dim();
+        for (index_t i = 0; i < c; ++i)
+          for (index_t j = 0; j < c; ++j) {
+            cplx acc = 0;
+            for (index_t k = 0; k < rows; ++k) acc += std::conj(t.data()[k * c + i]) * t.data()[k * c + j];
+            if (std::abs(acc - cplx(i == j ? 1.0 : 0.0)) > 1e-12) return false;
+          }
+      } else if (n > st.center()) {  // right unfolding b b^H = I
+        const index_t rows = t.left_dim(), c = t.phys_dim() * t.right_dim();
+        for (index_t i = 0; i < rows; ++i)
+          for (index_t j = 0; j < rows; ++j) {
+            cplx acc = 0;
+            for (index_t k = 0; k < c; ++k) acc += t.data()[i * c + k] * std::conj(t.data()[j * c + k]);
+            if (std::abs(acc - cplx(i == j ? 1.0 : 0.0)) > 1e-12) return false;
+          }
+      }
+    }
+    return true;
+  };
+  section("canonicalize: isometries at every centre (test_core.cpp:105-129)", [&] {
+    MPS state = random_uniform_mps(6, 2, 5, 42);
+    for (index_t center : {0, 2, 5}) {
+      auto c = canonicalize(state, center, NO_TRUNCATION);
+      CHECK(isometries_ok(c));
+    }
+    auto c3 = canonicalize(random_uniform_mps(8, 2, 8, 3), 3, NO_TRUNCATION.with_max_bond(4));
+    CHECK(isometries_ok(c3));
+  });
+  section("canonicalize(CanonicalMPS) at the same centre is unchanged (test_core.cpp:130-137)", [] {
+    MPS state = random_uniform_mps(5, 2, 4, 7);
+    auto c = canonicalize(state, 2, NO_TRUNCATION);
+    auto c2 = canonicalize(c, 2, NO_TRUNCATION);
+    CHECK(c2.center() == 2);
+    for (index_t n = 0; n < c.size(); ++n)
+      for (index_t i = 0; i < c[n].size(); ++i) CHECK(std::abs(c[n].data()[i] - c2[n].data()[i]) < 1e-14);
+    CHECK(c2.error() == c.error());  // recenter, not a new canonical pass (no floor added)
+  });
+  section("recenter back and forth leaves the vector invariant (test_core.cpp:148-155)", [&] {
+    MPS state = random_uniform_mps(6, 2, 4, 11);
+    auto exact = mps_to_dense(state);
+    auto c = canonicalize(state, 0, NO_TRUNCATION);
+    c.recenter(5, NO_TRUNCATION);
+    CHECK(c.center() == 5);
+    CHECK(isometries_ok(c));
+    c.recenter(0, NO_TRUNCATION);
+    CHECK(c.center() == 0);
+    CHECK(dist(mps_to_dense(c), exact) < 1e-12 * nrm(exact));
+    bool threw = false;
+    try {
+      c.recenter(6, NO_TRUNCATION);
+    } catch (const shape_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  });
+  section("truncating moves: error ledger and single moves (mps.hpp:238-279)", [&] {
+    MPS state = random_uniform_mps(8, 2, 8, 3);
+    auto exact = mps_to_dense(state);
+    auto c = canonicalize(state, 0, NO_TRUNCATION);
+    const double e0 = c.error();
+    const double w = c.move_center_right(NO_TRUNCATION.with_max_bond(4));
+    CHECK(c.center() == 1 && w > 0.0 && c.error() == e0);  // single moves do not touch the ledger
+    c.recenter(7, NO_TRUNCATION.with_max_bond(4));
+    CHECK(c.error() > e0);
+    CHECK(isometries_ok(c));
+    CHECK(dist(mps_to_dense(c), exact) <= c.error() + w + 1e-12);
+    const double wl = c.move_center_left(NO_TRUNCATION);
+    CHECK(c.center() == 6 && wl < 1e-12);
+    c.normalize_in_place();
+    CHECK(std::abs(c.norm() - 1.0) < 1e-14);
+  });
+  section("update_two_site / split_pair on the device (mps.hpp:164-173, 283-297)", [&] {
+    MPS state = random_uniform_mps(5, 2, 4, 17);
+    auto exact = mps_to_dense(state);
+    auto c = canonicalize(state, 1, NO_TRUNCATION);
+    Tensor3 joined = detail::join_pair(c[1], c[2]);
+    const double e = c.update_two_site(joined, SweepDirection::LEFT_TO_RIGHT, NO_TRUNCATION);
+    CHECK(c.center() == 2 && e < 1e-12);
+    CHECK(isometries_ok(c));
+    CHECK(dist(mps_to_dense(c), exact) < 1e-12 * nrm(exact));
+    joined = detail::join_pair(c[1], c[2]);
+    c.update_two_site(joined, SweepDirection::RIGHT_TO_LEFT, NO_TRUNCATION);
+    CHECK(c.center() == 1);
+    CHECK(isometries_ok(c));
+    CHECK(dist(mps_to_dense(c), exact) < 1e-12 * nrm(exact));
+    c.set_center(1);
+    c.set_tensor(1, c[1]);
+    bool threw = false;
+    try {
+      detail::split_pair(joined, 3, 2, NO_TRUNCATION, SweepDirection::LEFT_TO_RIGHT);
+    } catch (const shape_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  });
+  section("diag(v) w = v .* w (test_core.cpp:183-188, blas.hpp:70-83)", [] {
+    MPS v = random_uniform_mps(4, 2, 2, 22);
+    MPS w = random_uniform_mps(4, 2, 3, 23);
+    auto via_mpo = mps_to_dense(detail::apply_raw(mpo_from_diagonal_mps(v), w));
+    auto via_hadamard = mps_to_dense(hadamard(v, w));
+    CHECK(dist(via_mpo, via_hadamard) < 1e-12);
+    MPS e0 = basis_state(2, 2, 0);
+    MPO d = mpo_from_diagonal_mps(e0);
+    CHECK(d[0](0, 0, 0, 0) == cplx(1) && d[0](0, 1, 1, 0) == cplx(0) && d[0](0, 0, 1, 0) == cplx(0));
+  });
+  section("expectation_local on the device (test_blas.cpp:155-178)", [] {
+    Matrix sz(2, 2);
+    sz(0, 0) = 1.0;
+    sz(1, 1) = -1.0;
+    CHECK(std::abs(expectation_local(basis_state(3, 2, 0), sz, 0) - cplx(1)) < 1e-15);
+    CHECK(std::abs(expectation_local(basis_state(2, 2, 1), sz, 0, sz, 1) + cplx(1)) < 1e-15);
+    MPS v = random_uniform_mps(4, 2, 3, 16);
+    Matrix op(2, 2);
+    op(0, 1) = cplx(0.5, -1.0);
+    op(1, 0) = cplx(2.0, 0.25);
+    op(1, 1) = 0.75;
+    // dense reference: <v| op_2 |v>
+    auto dv = mps_to_dense(v);
+    cplx ref = 0;
+    for (index_t i = 0; i < 16; ++i)
+      for (index_t j = 0; j < 16; ++j) {
+        bool same = true;
+        for (int b = 0; b < 4; ++b)
+          if (b != 2 && (((i >> (3 - b)) & 1) != ((j >> (3 - b)) & 1))) same = false;
+        if (same) ref += std::conj(dv[i]) * op((i >> 1) & 1, (j >> 1) & 1) * dv[j];
+      }
+    CHECK(std::abs(expectation_local(v, op, 2) - ref) < 1e-12 * std::abs(ref));
+    bool threw = false;
+    try {
+      expectation_local(v, op, 1, op, 1);
+    } catch (const shape_error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  });
+  section("MPO / Tensor4 host algebra (mpo.hpp:42-92, tensor.hpp:113-142)", [] {
+    MPS v = random_uniform_mps(3, 2, 2, 31);
+    MPO a = mpo_from_diagonal_mps(v);
+    MPO h = a.adjoint();
+    CHECK(h.in_dimensions() == a.out_dimensions());
+    CHECK(h[1](0, 1, 1, 1) == std::conj(a[1](0, 1, 1, 1)));
+    MPO sc = a.scaled(cplx(0, 8.0));
+    CHECK(std::abs(sc[0](0, 1, 1, 1) - a[0](0, 1, 1, 1) * cplx(0, 2.0)) < 1e-14);
+    CHECK(std::abs(sc[2](1, 0, 0, 0) - a[2](1, 0, 0, 0) * 2.0) < 1e-14);
+    Tensor3 f = a[1].fuse_physical();
+    CHECK(f.phys_dim() == 4 && f(1, 3, 0) == a[1](1, 1, 1, 0));
+    Tensor4 back = Tensor4::split_physical(f, 2, 2);
+    CHECK(back(1, 1, 1, 0) == a[1](1, 1, 1, 0));
+    CHECK(a[1].conj()(0, 1, 1, 1) == std::conj(a[1](0, 1, 1, 1)));
+    Matrix blk = a[1].bond_block(0, 1);
+    CHECK(blk(1, 1) == a[1](0, 1, 1, 1));
+    MPS cj = v.conj();
+    CHECK(cj[0](0, 1, 1) == std::conj(v[0](0, 1, 1)));
+  });
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -237,3 +237,86 @@ def test_qr_precondition_small_rank_deficient():
     assert lib.ttg_debug_qr_pre(0, 128, 128, 0, _ptr(A), _ptr(Q), _ptr(RH), 1, None) == 0
     assert np.abs(Q.T @ Q - np.eye(128)).max() < 1e-13
     assert np.abs(Q @ RH.T - A).max() < 1e-12 * np.abs(A).max()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_svd_kept_negligible_values_orthonormal(dtype, mode, svd_impl):
+    """tol = 0 (NO_TRUNCATION) keeps numerically-zero singular values; their vectors
+    must still complete an orthonormal isometry (Eigen JacobiSVD semantics), so the
+    split reconstructs theta."""
+    rng = np.random.default_rng(21 + mode)
+    m, n, rank = 64, 48, 20
+    a, b = rng.standard_normal((m, rank)), rng.standard_normal((rank, n))
+    if dtype == np.complex128:
+        a = a + 1j * rng.standard_normal((m, rank))
+    th = a @ b
+    iso, sv, r, _ = _svd(th, mode, tol=0.0)
+    assert rank < r <= min(m, n)  # roundoff values are kept (strict > 0 cutoff)
+    assert sv[rank] < 1e-12 * sv[0]
+    if mode == 0:
+        assert np.abs(iso.conj().T @ iso - np.eye(r)).max() < 1e-12
+        assert np.abs(iso @ (iso.conj().T @ th) - th).max() < 1e-12 * sv[0]
+    else:
+        assert np.abs(iso @ iso.conj().T - np.eye(r)).max() < 1e-12
+        assert np.abs((th @ iso.conj().T) @ iso - th).max() < 1e-12 * sv[0]
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_svd_clustered_spectrum_isometry(n, svd_impl):
+    """Near-degenerate Schmidt spectra (blocks sigma = 1 +- 1e-9): the early stop must
+    not leave the isometry non-orthogonal."""
+    rng = np.random.default_rng(n)
+    U, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.repeat([1.0, 0.5, 0.1, 1e-3], n // 4) * (1 + 1e-9 * rng.standard_normal(n))
+    th = (U * s) @ V.T
+    for mode in (0, 1):
+        iso, sv, r, _ = _svd(th, mode, tol=1e-12)
+        if mode == 0:
+            assert np.abs(iso.conj().T @ iso - np.eye(r)).max() < 1e-12
+        else:
+            assert np.abs(iso @ iso.conj().T - np.eye(r)).max() < 1e-12
+        assert np.abs(sv - np.sort(s)[::-1]).max() < 1e-13
+
+
+_RETRY_SNIPPET = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from oracle import ttlab_oracle as O
+from paper_2601_16734_b200 import inputs as I, ttlab
+from tests._compare import dense, rel
+psi = I.random_mps(12, 2, 32, 101)
+strat = ttlab.Strategy(max_bond=12, max_sweeps=3)
+rep = []
+out = ttlab.simplify(psi, strat, report=rep)
+rr = {}
+ref = O.simplify(O.MPS(psi), O.Strategy(max_bond=12, max_sweeps=3), report=rr)
+assert out.bond_dimensions() == ref.bond_dimensions()
+assert rep[0]["sweeps"] == rr["sweeps"]
+assert abs(rep[0]["residual"] - rr["residual"]) < 1e-10
+assert rel(dense(out.to_tensors()), O.mps_to_dense(ref)) < 1e-10
+print("RETRY_OK")
+'''
+
+
+def test_svd_forced_retry_matches_oracle():
+    """schmidt.hpp:23-35: a split that fails its first attempt is jittered by
+    1e-14 |theta| and retried.  TTG_SVD_FORCE_RETRY=1 caps the first attempt at one
+    Jacobi sweep, so every split takes the retry path; the result must still match
+    the oracle (the jitter is far below the 1e-10 parity tolerance)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TTG_SVD_FORCE_RETRY="1")
+    r = subprocess.run([sys.executable, "-c", _RETRY_SNIPPET], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "RETRY_OK" in r.stdout, r.stdout + r.stderr
+    env2 = dict(os.environ, TTG_SVD_FORCE_RETRY="1")
+    snippet = ("import sys, numpy as np; sys.path.insert(0, '.'); from tests.test_gpu_kernels import _svd; "
+               "th = np.random.default_rng(5).standard_normal((40, 40)); iso, sv, r, e2 = _svd(th, 0); "
+               "ref = np.linalg.svd(th, compute_uv=False); assert np.abs(sv - ref).max() < 1e-12 * ref[0]; "
+               "assert np.abs(iso.T @ iso - np.eye(r)).max() < 1e-12; print('SVD_RETRY_OK')")
+    r = subprocess.run([sys.executable, "-c", snippet], cwd=root, env=env2, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "SVD_RETRY_OK" in r.stdout, r.stdout + r.stderr
