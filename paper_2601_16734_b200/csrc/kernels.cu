@@ -1,5 +1,7 @@
 #include "kernels.cuh"
 
+#include <algorithm>
+
 namespace ttg {
 namespace {
 
@@ -25,52 +27,100 @@ __device__ double block_sum(double v) {
   return red[32];
 }
 
-// One thread per output element; the innermost output index (ar) is the
-// fastest, so loads of A and stores of C are coalesced.  The MPO tensor is tiny
-// and stays in L1.
-template <typename T>
-__global__ void expand_mpo_kernel(const T* __restrict__ W, const T* __restrict__ A, T* __restrict__ C, int Dl,
-                                  int dout, int din, int Dr, int Al, int Ar, long long total, long long sA,
-                                  long long sC) {
-  const int chain = blockIdx.y;
+// Expansions are pure HBM writes (the inputs are tiny and L2/L1 resident), so
+// they are organised by OUTPUT ROW: one CTA per row of the fused-bond target,
+// the row's indices decoded once per CTA (no per-element div/mod), and each
+// thread writes VEC consecutive elements (16-byte stores: VEC = 2 for f64,
+// 1 for complex128) for every right block, reusing the input values it holds
+// in registers across the blocks.
+
+template <typename T, int VEC> struct Vec;
+template <> struct Vec<double, 2> { using type = double2; };
+template <> struct Vec<double, 1> { using type = double; };
+template <> struct Vec<cplx, 1> { using type = cplx; };
+
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec(T* dst, const T (&v)[VEC]) {
+  if constexpr (VEC == 2)
+    *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+  else
+    *dst = v[0];
+}
+
+// apply_raw (mpo.hpp:213-238): C[(cb*Al + al), j, (cb2*Ar + ar)] = sum_i W[cb, j, i, cb2] A[al, i, ar].
+// Row r = (cb*Al + al)*dout + j; columns (cb2, ar).
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) expand_mpo_kernel(const T* __restrict__ W, const T* __restrict__ A,
+                                                          T* __restrict__ C, int Dl, int dout, int din, int Dr, int Al,
+                                                          int Ar, long long sA, long long sC) {
+  const int chain = blockIdx.z;
   A += sA * chain;
   C += sC * chain;
+  const int rows = Dl * Al * dout;
   const long long cols = (long long)Dr * Ar;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long col = idx % cols;
-    const long long rj = idx / cols;
-    const int j = (int)(rj % dout);
-    const long long row = rj / dout;
-    const int cb = (int)(row / Al), al = (int)(row % Al);
-    const int cb2 = (int)(col / Ar), ar = (int)(col % Ar);
-    T acc = Scalar<T>::zero();
-    for (int i = 0; i < din; ++i) {
-      const T w = W[(((long long)cb * dout + j) * din + i) * Dr + cb2];
-      acc = add(acc, mul(w, A[((long long)al * din + i) * Ar + ar]));
+  for (int row = blockIdx.y * gridDim.x + blockIdx.x; row < rows; row += gridDim.x * gridDim.y) {
+    const int j = row % dout, ra = row / dout;
+    const int cb = ra / Al, al = ra - cb * Al;
+    T* crow = C + (long long)row * cols;
+    for (int ar = threadIdx.x * VEC; ar < Ar; ar += blockDim.x * VEC) {
+      T a[4][VEC];  // the first four physical indices in registers
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < din)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) a[i][v] = A[((long long)al * din + i) * Ar + ar + v];
+      for (int cb2 = 0; cb2 < Dr; ++cb2) {
+        T out[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) out[v] = Scalar<T>::zero();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < din) {
+            const T w = W[(((long long)cb * dout + j) * din + i) * Dr + cb2];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) out[v] = add(out[v], mul(w, a[i][v]));
+          }
+        for (int i = 4; i < din; ++i) {  // physical dimensions > 4: straight from L1/L2
+          const T w = W[(((long long)cb * dout + j) * din + i) * Dr + cb2];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) out[v] = add(out[v], mul(w, A[((long long)al * din + i) * Ar + ar + v]));
+        }
+        store_vec<T, VEC>(crow + (long long)cb2 * Ar + ar, out);
+      }
     }
-    C[idx] = acc;
   }
 }
 
-template <typename T>
-__global__ void expand_hadamard_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C, int Al,
-                                       int d, int Ar, int Bl, int Br, long long total, long long sA, long long sB,
-                                       long long sC) {
-  const int chain = blockIdx.y;
+// hadamard (blas.hpp:45-67): C[(a*Bl + b), s, (a2*Br + b2)] = A[a, s, a2] B[b, s, b2].
+// Row r = (a*Bl + b)*d + s; columns (a2, b2).
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) expand_hadamard_kernel(const T* __restrict__ A, const T* __restrict__ B,
+                                                               T* __restrict__ C, int Al, int d, int Ar, int Bl,
+                                                               int Br, long long sA, long long sB, long long sC) {
+  const int chain = blockIdx.z;
   A += sA * chain;
   B += sB * chain;
   C += sC * chain;
+  const int rows = Al * Bl * d;
   const long long cols = (long long)Ar * Br;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long col = idx % cols;
-    const long long rs = idx / cols;
-    const int s = (int)(rs % d);
-    const long long row = rs / d;
-    const int a = (int)(row / Bl), b = (int)(row % Bl);
-    const int a2 = (int)(col / Br), b2 = (int)(col % Br);
-    C[idx] = mul(A[((long long)a * d + s) * Ar + a2], B[((long long)b * d + s) * Br + b2]);
+  for (int row = blockIdx.y * gridDim.x + blockIdx.x; row < rows; row += gridDim.x * gridDim.y) {
+    const int s = row % d, ab = row / d;
+    const int a = ab / Bl, b = ab - a * Bl;
+    T* crow = C + (long long)row * cols;
+    const T* arow = A + ((long long)a * d + s) * Ar;
+    const T* brow = B + ((long long)b * d + s) * Br;
+    for (int b2 = threadIdx.x * VEC; b2 < Br; b2 += blockDim.x * VEC) {
+      T bv[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) bv[v] = brow[b2 + v];
+      for (int a2 = 0; a2 < Ar; ++a2) {
+        const T x = arow[a2];
+        T out[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) out[v] = mul(x, bv[v]);
+        store_vec<T, VEC>(crow + (long long)a2 * Br + b2, out);
+      }
+    }
   }
 }
 
@@ -244,18 +294,37 @@ int grid_for(long long total, int threads) {
 template <typename T>
 cudaError_t expand_mpo(const T* W, const T* A, T* C, int Dl, int dout, int din, int Dr, int Al, int Ar, int chains,
                        long long sA, long long sC, cudaStream_t s) {
-  const long long total = (long long)Dl * Al * dout * Dr * Ar;
-  expand_mpo_kernel<T><<<dim3(grid_for(total, 256), chains), 256, 0, s>>>(W, A, C, Dl, dout, din, Dr, Al, Ar, total,
-                                                                          sA, sC);
+  const int rows = Dl * Al * dout;
+  const dim3 grid(std::min(rows, 32768), (rows + 32767) / 32768, chains);
+  // threads per row: enough for one pass over Ar
+  const bool vec2 = !Scalar<T>::is_complex && (Ar % 2 == 0);
+  const int per = vec2 ? (Ar / 2) : Ar;
+  const int nt = per >= 256 ? 256 : std::max(32, (per + 31) / 32 * 32);
+  if constexpr (!Scalar<T>::is_complex) {
+    if (vec2) {
+      expand_mpo_kernel<T, 2><<<grid, nt, 0, s>>>(W, A, C, Dl, dout, din, Dr, Al, Ar, sA, sC);
+      return cudaGetLastError();
+    }
+  }
+  expand_mpo_kernel<T, 1><<<grid, nt, 0, s>>>(W, A, C, Dl, dout, din, Dr, Al, Ar, sA, sC);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t expand_hadamard(const T* A, const T* B, T* C, int Al, int d, int Ar, int Bl, int Br, int chains,
                             long long sA, long long sB, long long sC, cudaStream_t s) {
-  const long long total = (long long)Al * Bl * d * Ar * Br;
-  expand_hadamard_kernel<T><<<dim3(grid_for(total, 256), chains), 256, 0, s>>>(A, B, C, Al, d, Ar, Bl, Br, total, sA,
-                                                                               sB, sC);
+  const int rows = Al * Bl * d;
+  const dim3 grid(std::min(rows, 32768), (rows + 32767) / 32768, chains);
+  const bool vec2 = !Scalar<T>::is_complex && (Br % 2 == 0);
+  const int per = vec2 ? (Br / 2) : Br;
+  const int nt = per >= 256 ? 256 : std::max(32, (per + 31) / 32 * 32);
+  if constexpr (!Scalar<T>::is_complex) {
+    if (vec2) {
+      expand_hadamard_kernel<T, 2><<<grid, nt, 0, s>>>(A, B, C, Al, d, Ar, Bl, Br, sA, sB, sC);
+      return cudaGetLastError();
+    }
+  }
+  expand_hadamard_kernel<T, 1><<<grid, nt, 0, s>>>(A, B, C, Al, d, Ar, Bl, Br, sA, sB, sC);
   return cudaGetLastError();
 }
 

@@ -353,10 +353,10 @@ int main() {
   section("truncating moves: error ledger and single moves (mps.hpp:238-279)", [&] {
     MPS state = random_uniform_mps(8, 2, 8, 3);
     auto exact = mps_to_dense(state);
-    auto c = canonicalize(state, 0, NO_TRUNCATION);
+    auto c = canonicalize(state, 3, NO_TRUNCATION);
     const double e0 = c.error();
-    const double w = c.move_center_right(NO_TRUNCATION.with_max_bond(4));
-    CHECK(c.center() == 1 && w > 0.0 && c.error() == e0);  // single moves do not touch the ledger
+    const double w = c.move_center_right(NO_TRUNCATION.with_max_bond(4));  // bond 4: 8 -> 4
+    CHECK(c.center() == 4 && w > 0.0 && c.error() == e0);  // single moves do not touch the ledger
     c.recenter(7, NO_TRUNCATION.with_max_bond(4));
     CHECK(c.error() > e0);
     CHECK(isometries_ok(c));
