@@ -355,9 +355,10 @@ struct Engine {
       CK(cudaMemsetAsync(ctx->d_sweeps, 0, B * sizeof(int), st));
       p.sweeps_out = B <= 4096 ? ctx->d_sweeps : nullptr;
     }
-    // kept numerically-zero singular values (sigma <= l eps |theta|_F <= l sqrt(k) eps sigma_0) are
-    // possible only when tol < l sqrt(k) eps: then the isometry is completed after the sweeps
-    const bool complete = svals && std::min(l, k) <= svals_cap && tol < (double)l * std::sqrt((double)k) * 2.3e-16 &&
+    // kept near-zero singular values (sigma <= 100 l eps |theta|_F <= 100 l sqrt(k) eps sigma_0, see
+    // iso_complete) are possible only when tol < 100 l sqrt(k) eps: then the isometry is checked and
+    // completed after the sweeps
+    const bool complete = svals && std::min(l, k) <= svals_cap && tol < 100.0 * l * std::sqrt((double)k) * 2.3e-16 &&
                           iso_complete_smem(l, std::min(l, k), sizeof(T)) <= 200 * 1024;
     if (complete) {
       p.svals = svals;
@@ -467,6 +468,46 @@ void Engine<T>::split_large(const void* theta, long long s_theta, DimExpr M, Dim
   const int m = M.eval(hb.data(), 0, ld), n = N.eval(hb.data(), 0, ld);
   const int l = mode == 0 ? m : n, k = mode == 0 ? n : m, r0 = std::min(l, k);
   const size_t es = sizeof(T);
+  static const int single = [] {
+    const char* e = getenv("TTG_PRE");
+    return e ? atoi(e) == 1 : 0;
+  }();
+  if (single) {
+    // One R-only QR: mode 0: theta^H = Q R, theta = R^H Q^H, so the left singular vectors of
+    // theta are those of L = R^H (m x r0): Jacobi mode 0 on L writes U_r straight into iso.
+    // mode 1: theta = Q R, the right singular vectors of theta are those of R (r0 x n): Jacobi
+    // mode 1 on R writes V_r^H straight into iso.  No Q, no isometry GEMM.
+    const int rr = std::min(m, n);
+    DevBuf Mb((size_t)m * n * es, st), R((size_t)rr * std::max(m, n) * es, st), Lb((size_t)rr * std::max(m, n) * es, st);
+    const int qr_rows = mode == 0 ? n : m, qr_cols = mode == 0 ? m : n;
+    if (mode == 0)
+      CK(conj_transpose<T>(theta, 0, m, n, Mb.p, 0, 1, st));
+    else
+      CK(cudaMemcpyAsync(Mb.p, theta, (size_t)m * n * es, cudaMemcpyDeviceToDevice, st));
+    ++ctx->launches;
+    {
+      size_t a, v, t2, w2, pp;
+      qr_blocked_elems<T>(qr_rows, qr_cols, &a, &v, &t2, &w2, &pp);
+      DevBuf wa(a * es, st), wv(v * es, st), wt(t2 * es, st), w1b(w2 * es, st), w2b(w2 * es, st), wp(pp * es, st);
+      QrParams qp{Mb.p, 0, nullptr, 0, R.p, 0, nullptr, 0, qr_rows, qr_cols};
+      const QrBlockedWork qw{wa.p, wv.p, wt.p, w1b.p, w2b.p, wp.p, 0, 0, 0, 0, 0};
+      long long nl = 0;
+      const double big = std::max(qr_rows, qr_cols), sm = std::min(qr_rows, qr_cols);
+      ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * 2.0 * sm * sm * (big - sm / 3.0));
+      CK(householder_qr_blocked<T>(qp, qw, 1, st, &nl));
+      ctx->launches += nl;
+    }
+    if (mode == 0) {  // L = R^H (m x rr)
+      CK(conj_transpose<T>(R.p, 0, rr, m, Lb.p, 0, 1, st));
+      ++ctx->launches;
+      S(Lb.p, 0, dconst(m), dconst(rr), out_idx, iso, 0, 0, tol, max_bond, check_active, accumulate, work, s_work,
+        Warm(), true);
+    } else {
+      S(R.p, 0, dconst(rr), dconst(n), out_idx, iso, 0, 1, tol, max_bond, check_active, accumulate, work, s_work,
+        Warm(), true);
+    }
+    return;
+  }
   DevBuf Mb((size_t)l * k * es, st), Q1((size_t)l * r0 * es, st), R1((size_t)r0 * k * es, st),
       R1h((size_t)k * r0 * es, st), R2((size_t)r0 * r0 * es, st), Ut((size_t)r0 * r0 * es, st);
   if (mode == 0)
@@ -632,6 +673,17 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   T* cbuf[2] = {C0.as<T>(), C1.as<T>()};
   const double tol = s.tolerance;
 
+  // TTG_PHASES=1: device time of the call's phases on stderr (diagnostics)
+  static const bool phases = getenv("TTG_PHASES") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  auto mark = [&](const char* name) {
+    if (!phases) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.emplace_back(name, e);
+  };
+  mark("start");
   // ---- pass 1: exact left-to-right QR (mps.hpp:193-205)
   int cur = 0;
   const T* curp = static_cast<const T*>(guess.site[0]);
@@ -727,6 +779,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   CK(cudaMemsetAsync(fmeta.p, 0, (size_t)2 * B * L * sizeof(int), st));
   int* fU = fmeta.as<int>();
   int* fV = fU + (size_t)B * L;
+  mark("qr_pass");
   // ---- pass 2: truncating right-to-left sweep (mps.hpp:206-210, 253-265)
   for (int k = L - 1; k >= 1; --k) {
     const DimExpr rows = dconst(q[k]);
@@ -767,6 +820,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   const int out_center = variational ? 0 : center;
 
   if (variational && L >= 2) {
+    mark("truncating_pass");
     // ---- environments (simplify.hpp:28-36)
     std::vector<DevBuf> lenv, renv;
     lenv.reserve(L + 1);
@@ -797,6 +851,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     for (int k = 0; k < L; ++k) bound[L + 2] = std::max({bound[L + 2], d[k] * pb[k], d[k] * pb[k + 1]});
     ++ctx->launches;
 
+    mark("right_envs");
     // ---- sweeps (simplify.hpp:66-91, 114-125)
     const int nsweeps = std::max(1, s.max_sweeps);
     std::vector<ChainState> hstate(B);
@@ -872,6 +927,16 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
                          cudaMemcpyDeviceToDevice, st));
   }
 
+  mark("sweeps");
+  if (phases) {
+    cudaEventSynchronize(marks.back().second);
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+      fprintf(stderr, "phase %-16s %9.2f ms\n", marks[i].first, ms);
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
   // ---- finalize: norms, ledger, zero states, normalisation
   DevBuf norms((size_t)B * sizeof(double), st);
   {

@@ -71,3 +71,35 @@ def test_recenter_exact_and_truncating():
     assert rel(dense(moved.to_tensors()), O.mps_to_dense(ref)) <= 1e-10
     with pytest.raises(t.ShapeError):
         t.recenter(c, 8, t.NO_TRUNCATION)
+
+
+def test_mps_from_device_validates_and_copies():
+    """ttg_mps_from_device: device buffers (torch tensors on another stream) are copied before
+    the call returns; bad dtype / shapes / errors are rejected."""
+    import torch
+    t = T()
+    from paper_2601_16734_b200 import _lib
+    psi = [np.random.default_rng(k).standard_normal(s) for k, s in enumerate([(1, 2, 3), (3, 2, 4), (4, 2, 1)])]
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        dev = [torch.from_numpy(a.copy()).cuda(non_blocking=True) for a in psi]
+    bonds, phys = [1, 3, 4, 1], [2, 2, 2]
+    m = t.DeviceMPS.from_device(3, _lib.TTG_F64, 1, bonds, phys, [d.data_ptr() for d in dev], [0.5])
+    for d in dev:
+        d.fill_(float("nan"))  # the copy is complete: overwriting the sources must not matter
+    torch.cuda.synchronize()
+    got = m.to_tensors()
+    for a, b in zip(got, psi):
+        assert np.array_equal(a, b)
+    assert m.error() == 0.5
+    ptrs = [d.data_ptr() for d in dev]
+    with pytest.raises(Exception):
+        t.DeviceMPS.from_device(3, 7, 1, bonds, phys, ptrs)  # unknown dtype
+    with pytest.raises(t.ShapeError):
+        t.DeviceMPS.from_device(3, _lib.TTG_F64, 1, [1, 0, 4, 1], phys, ptrs)
+    with pytest.raises(t.ShapeError):
+        t.DeviceMPS.from_device(3, _lib.TTG_F64, 1, bonds, phys, ptrs, [-1.0])
+    with pytest.raises(t.ShapeError):  # scprod of states with different physical dimensions
+        u = t.DeviceMPS.from_tensors([np.ones((1, 2, 1)), np.ones((1, 3, 1))])
+        v = t.DeviceMPS.from_tensors([np.ones((1, 2, 1)), np.ones((1, 2, 1))])
+        t.scprod(u, v)

@@ -131,3 +131,19 @@ def test_config5_batch_parity():
         assert abs(rep[i]["residual"] - rr["residual"]) <= TOL * tn
         assert abs(rep[i]["norm"] - ref.norm()) <= TOL * ref.norm()
         assert rel(dense(ts), O.mps_to_dense(ref)) <= TOL
+
+
+def test_config4_repeat_bitwise():
+    """Deterministic reductions (split-K partials reduced in fixed order): two C4 calls give
+    bitwise identical outputs and reports."""
+    t = T()
+    cfg = I.CONFIGS["C4"]
+    (psi,), W = I.config_inputs(cfg)
+    strat = t.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
+    Wd, pd = t.DeviceMPO(W), t.DeviceMPS.from_tensors(psi)
+    r1, r2 = [], []
+    a = t.apply(Wd, pd, strat, report=r1).to_tensors()
+    b = t.apply(Wd, pd, strat, report=r2).to_tensors()
+    assert r1 == r2
+    for x, y in zip(a, b):
+        assert x.shape == y.shape and np.array_equal(x, y)
