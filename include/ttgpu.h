@@ -193,6 +193,19 @@ ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* op, const char* path);
  * [D0][chiAo][chiA], R[c2](b', B) as [D2][chiBo][chiB], x[a][s1][s2][B], y[a'][s1'][s2'][b']. */
 ttg_status ttg_apply_effective_two_site(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
                                         const void* W2, const void* R, const void* x, void* y);
+/* Device-pointer variant of ttg_apply_effective_two_site: L, W1, W2, R, x, y are device buffers with
+ * the same layouts; stream-ordered on the context stream and NOT synchronised at return (a Lanczos
+ * loop chains calls without host round trips; ttg_synchronize waits). */
+ttg_status ttg_apply_effective_two_site_dev(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
+                                            const void* W2, const void* R, const void* x, void* y);
+/* detail::update_left_op_environment (side TTG_LEFT_TO_RIGHT) / update_right_op_environment
+ * (TTG_RIGHT_TO_LEFT) of environments.hpp:42-83 on device buffers (stream-ordered, not synchronised).
+ * dims = {Dl, dout, din, Dr, bra_l, bra_r, ket_l, ket_r}: bra (Tensor3 bra_l x dout x bra_r),
+ * op (Tensor4 Dl x dout x din x Dr), ket (Tensor3 ket_l x din x ket_r).  Environments are stacked
+ * matrices E[c](a, b) stored [c][a][b]: left: env Dl x bra_l x ket_l -> out Dr x bra_r x ket_r;
+ * right: env Dr x bra_r x ket_r -> out Dl x bra_l x ket_l. */
+ttg_status ttg_op_env_update(ttg_ctx* ctx, int dtype, int side, const int* dims, const void* env, const void* bra,
+                             const void* op, const void* ket, void* out);
 /* blas.hpp:128-138 expectation_mpo(op, u, v) = <u, op v> per chain (v NULL: v = u). */
 ttg_status ttg_expectation_mpo(ttg_ctx* ctx, const ttg_dmpo* op, const ttg_dmps* u, const ttg_dmps* v, double* out_re,
                                double* out_im);

@@ -468,9 +468,12 @@ void Engine<T>::split_large(const void* theta, long long s_theta, DimExpr M, Dim
   const int m = M.eval(hb.data(), 0, ld), n = N.eval(hb.data(), 0, ld);
   const int l = mode == 0 ? m : n, k = mode == 0 ? n : m, r0 = std::min(l, k);
   const size_t es = sizeof(T);
+  // TTG_PRE=2: the two-QR preconditioner below.  Default: one R-only QR (C4 A/B on one B200:
+  // 3029 -> 2715 ms per call with the CTA-pair grid kernel; the Jacobi needs ~13% more sweeps
+  // on L = R^H than on R2^H, the second QR with its explicit Q costs more than that)
   static const int single = [] {
     const char* e = getenv("TTG_PRE");
-    return e ? atoi(e) == 1 : 0;
+    return e ? atoi(e) != 2 : 1;
   }();
   if (single) {
     // One R-only QR: mode 0: theta^H = Q R, theta = R^H Q^H, so the left singular vectors of
@@ -684,6 +687,19 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     marks.emplace_back(name, e);
   };
   mark("start");
+  // Q-free exact pass (single chains, two-level blocked QRs): the thin Q of site k is applied to
+  // the carried U S of pass 2 from its WY form (4 m k r flops) instead of being formed (2 m k^2)
+  // and multiplied (2 m k r).  TTG_QFREE=0 forms Q as before.
+  static const bool qfree_ok = [] {
+    const char* e = getenv("TTG_QFREE");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<char> qfree(L, 0);
+  std::vector<DevBuf> wy(L);
+  for (int k = 0; k + 1 < L; ++k)
+    qfree[k] = qfree_ok && B == 1 && (long long)qr_workspace_elems<T>(q[k] * d[k], g[k + 1]) * (long long)sizeof(T) >
+                                           200 * 1024 && qr_two_level(q[k] * d[k], g[k + 1]) &&
+               q[k + 1] == std::min(q[k] * d[k], g[k + 1]);
   // ---- pass 1: exact left-to-right QR (mps.hpp:193-205)
   int cur = 0;
   const T* curp = static_cast<const T*>(guess.site[0]);
@@ -710,7 +726,22 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
       ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * B * 4.0 * b * b * (a - b / 3.0));
       if ((long long)qr_workspace_elems<T>(qp.m, qp.n) * (long long)sizeof(T) > 200 * 1024) {
         long long nl = 0;
-        CK(householder_qr_blocked<T>(qp, qbw, B, st, &nl));
+        if (qfree[k]) {
+          // Q is never formed: the reflectors stay in the psi site (ld = q_{k+1} = min(m, n)) and the
+          // WY factors in wy[k]; pass 2 applies Q to the carried U S (householder_apply_q)
+          size_t a_, v_, t_, w_, p_;
+          qr_blocked_elems<T>(qp.m, qp.n, &a_, &v_, &t_, &w_, &p_);
+          wy[k] = DevBuf(t_ * sizeof(T), st);
+          QrBlockedWork wk = qbw;
+          wk.V = psi->site[k];
+          wk.T = wy[k].p;
+          wk.keep_wy = 1;
+          QrParams qr = qp;
+          qr.Q = nullptr;
+          CK(householder_qr_blocked<T>(qr, wk, B, st, &nl));
+        } else {
+          CK(householder_qr_blocked<T>(qp, qbw, B, st, &nl));
+        }
         ctx->launches += nl - 1;
       } else {
         CK(householder_qr<T>(qp, B, st));
@@ -789,8 +820,23 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     E.G(curp, s_cur, psi->site[k], P.psi_cap[k], Bb.p, sBb, rows, dbond(k), cols, OP_N, OP_C, false);
     // prev.left_matrix() * (U S)  (mps.hpp:261)
     const int nxt = cur ^ 1;
-    E.G(psi->site[k - 1], P.psi_cap[k - 1], Bb.p, sBb, cbuf[nxt], sC, dconst(q[k - 1] * d[k - 1]), dbond(k),
-        dconst(q[k]), OP_N, OP_N, false);
+    if (qfree[k - 1]) {  // Q_{k-1} [U S; 0] from the WY form of the exact-pass QR
+      int r = 0;
+      CK(cudaMemcpyAsync(&r, E.d_bonds + k, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const int mq = q[k - 1] * d[k - 1];
+      T* X = cbuf[nxt];
+      CK(cudaMemcpyAsync(X, Bb.p, (size_t)q[k] * r * es, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemsetAsync(X + (size_t)q[k] * r, 0, (size_t)(mq - q[k]) * r * es, st));
+      long long nl = 0;
+      ProfScope ps(ctx, TTG_PROF_GEMM, (Scalar<T>::is_complex ? 16.0 : 4.0) * mq * (double)q[k] * r);
+      CK(householder_apply_q<T>(psi->site[k - 1], wy[k - 1].p, mq, q[k], X, r, qbW1.p, qbW2.p, st, &nl));
+      ctx->launches += nl;
+      wy[k - 1] = DevBuf();
+    } else {
+      E.G(psi->site[k - 1], P.psi_cap[k - 1], Bb.p, sBb, cbuf[nxt], sC, dconst(q[k - 1] * d[k - 1]), dbond(k),
+          dconst(q[k]), OP_N, OP_N, false);
+    }
     cur = nxt;
     curp = cbuf[cur];
     s_cur = sC;
@@ -2099,6 +2145,49 @@ __global__ void heff_mix_kernel(const T* XL, const T* W1, const T* W2, T* V, int
   }
 }
 
+// y = H_eff x on device buffers (stream-ordered, no host synchronisation).
+template <typename T>
+void heff_two_site_dev(ttg_ctx* ctx, const int* dm, const void* L, const void* W1, const void* W2, const void* R,
+                       const void* x, void* y) {
+  const int D0 = dm[0], D1 = dm[1], D2 = dm[2], d1o = dm[3], d1 = dm[4], d2o = dm[5], d2 = dm[6];
+  const int chiAo = dm[7], chiA = dm[8], chiBo = dm[9], chiB = dm[10];
+  cudaStream_t st = ctx->stream;
+  const size_t es = sizeof(T);
+  const size_t nW1 = (size_t)D0 * d1o * d1 * D1, nW2 = (size_t)D1 * d2o * d2 * D2;
+  const size_t nXL = (size_t)D0 * chiAo * d1 * d2 * chiB, nV = (size_t)chiAo * d1o * d2o * D2 * chiB;
+  DevBuf XL(nXL * es, st), V(nV * es, st);
+  // XL = [L[0]; ...; L[D0-1]] x  ((D0 chiAo) x chiA times chiA x (d1 d2 chiB))
+  const int M1 = D0 * chiAo, N1 = d1 * d2 * chiB;
+  GemmParams g1{L, x, XL.p, 0, 0, 0, dconst(M1), dconst(N1), dconst(chiA), nullptr, 0, nullptr, 1.0, 0};
+  {
+    ProfScope ps(ctx, TTG_PROF_GEMM, (Scalar<T>::is_complex ? 8.0 : 2.0) * M1 * (double)N1 * chiA);
+    CK(gemm<T>(g1, OP_N, OP_N, M1, N1, 1, st, chiA));
+  }
+  const size_t smem = (nW1 + nW2) * es;
+  if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
+  const long long tot = (long long)nV;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256));
+  {
+    ProfScope ps(ctx, TTG_PROF_EXPAND);
+    heff_mix_kernel<T><<<blocks, 256, smem, st>>>(static_cast<const T*>(XL.p), static_cast<const T*>(W1),
+                                                   static_cast<const T*>(W2), static_cast<T*>(V.p), D0, D1, D2, d1o,
+                                                   d1, d2o, d2, chiAo, chiB);
+    CK(cudaGetLastError());
+  }
+  // y += V[:, c2, :] R[c2]^T for every c2  ((chiAo d1o d2o) x chiB times chiB x chiBo)
+  const int M3 = chiAo * d1o * d2o;
+  for (int c2 = 0; c2 < D2; ++c2) {
+    GemmParams g3{static_cast<const T*>(V.p) + (size_t)c2 * chiB, static_cast<const T*>(R) + (size_t)c2 * chiBo * chiB,
+                  y, 0, 0, 0, dconst(M3), dconst(chiBo), dconst(chiB), nullptr, 0, nullptr, 1.0, c2 > 0 ? 1 : 0};
+    g3.lda = (long long)D2 * chiB;
+    g3.ldb = chiB;
+    g3.ldc = chiBo;
+    ProfScope ps(ctx, TTG_PROF_GEMM, (Scalar<T>::is_complex ? 8.0 : 2.0) * M3 * (double)chiBo * chiB);
+    CK(gemm<T>(g3, OP_N, OP_T, M3, chiBo, 1, st, chiB));
+  }
+  ctx->launches += 2 + D2;
+}
+
 template <typename T>
 void heff_two_site(ttg_ctx* ctx, const int* dm, const void* hL, const void* hW1, const void* hW2, const void* hR,
                    const void* hx, void* hy) {
@@ -2108,43 +2197,149 @@ void heff_two_site(ttg_ctx* ctx, const int* dm, const void* hL, const void* hW1,
   const size_t es = sizeof(T);
   const size_t nL = (size_t)D0 * chiAo * chiA, nW1 = (size_t)D0 * d1o * d1 * D1, nW2 = (size_t)D1 * d2o * d2 * D2;
   const size_t nR = (size_t)D2 * chiBo * chiB, nx = (size_t)chiA * d1 * d2 * chiB;
-  const size_t nXL = (size_t)D0 * chiAo * d1 * d2 * chiB, nV = (size_t)chiAo * d1o * d2o * D2 * chiB;
   const size_t ny = (size_t)chiAo * d1o * d2o * chiBo;
-  DevBuf L(nL * es, st), W1(nW1 * es, st), W2(nW2 * es, st), R(nR * es, st), X(nx * es, st), XL(nXL * es, st),
-      V(nV * es, st), Y(ny * es, st);
+  DevBuf L(nL * es, st), W1(nW1 * es, st), W2(nW2 * es, st), R(nR * es, st), X(nx * es, st), Y(ny * es, st);
   CK(cudaMemcpyAsync(L.p, hL, nL * es, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(W1.p, hW1, nW1 * es, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(W2.p, hW2, nW2 * es, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(R.p, hR, nR * es, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(X.p, hx, nx * es, cudaMemcpyHostToDevice, st));
-  // XL = [L[0]; ...; L[D0-1]] x  ((D0 chiAo) x chiA times chiA x (d1 d2 chiB))
-  const int M1 = D0 * chiAo, N1 = d1 * d2 * chiB;
-  GemmParams g1{L.p, X.p, XL.p, 0, 0, 0, dconst(M1), dconst(N1), dconst(chiA), nullptr, 0, nullptr, 1.0, 0};
-  CK(gemm<T>(g1, OP_N, OP_N, M1, N1, 1, st, chiA));
-  const size_t smem = (nW1 + nW2) * es;
-  if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
-  const long long tot = (long long)nV;
-  const int blocks = (int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256));
-  heff_mix_kernel<T><<<blocks, 256, smem, st>>>(static_cast<const T*>(XL.p), static_cast<const T*>(W1.p),
-                                                 static_cast<const T*>(W2.p), static_cast<T*>(V.p), D0, D1, D2, d1o,
-                                                 d1, d2o, d2, chiAo, chiB);
-  CK(cudaGetLastError());
-  // y += V[:, c2, :] R[c2]^T for every c2  ((chiAo d1o d2o) x chiB times chiB x chiBo)
-  const int M3 = chiAo * d1o * d2o;
-  for (int c2 = 0; c2 < D2; ++c2) {
-    GemmParams g3{static_cast<const T*>(V.p) + (size_t)c2 * chiB, static_cast<const T*>(R.p) + (size_t)c2 * chiBo * chiB,
-                  Y.p, 0, 0, 0, dconst(M3), dconst(chiBo), dconst(chiB), nullptr, 0, nullptr, 1.0, c2 > 0 ? 1 : 0};
-    g3.lda = (long long)D2 * chiB;
-    g3.ldb = chiB;
-    g3.ldc = chiBo;
-    CK(gemm<T>(g3, OP_N, OP_T, M3, chiBo, 1, st, chiB));
-  }
-  ctx->launches += 2 + D2;
+  heff_two_site_dev<T>(ctx, dm, L.p, W1.p, W2.p, R.p, X.p, Y.p);
   CK(cudaMemcpyAsync(hy, Y.p, ny * es, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 }
+
+// Operator-environment mixing (memory-bound, W in shared memory).
+// left:  Y[c'][a][s'][b'] = sum_{c,s} W[c,s',s,c'] X[c][a][s][b']          (X: D x P x d x Q)
+// right: Y[c][s'][a'][b] = sum_{c',s} W[c,s',s,c'] Z[c'][a'][b][s]          (Z: D' x P x Q x d)
+template <typename T, bool LEFT>
+__global__ void openv_mix_kernel(const T* X, const T* W, T* Y, int Dl, int dout, int din, int Dr, int P, int Q) {
+  extern __shared__ __align__(16) unsigned char openv_smem[];
+  T* w = reinterpret_cast<T*>(openv_smem);
+  const int nw = Dl * dout * din * Dr;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) w[i] = W[i];
+  __syncthreads();
+  const int Dout = LEFT ? Dr : Dl, Din = LEFT ? Dl : Dr;
+  const long long total = (long long)Dout * P * dout * Q;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    int co, p, sp, q;
+    if constexpr (LEFT) {  // idx = ((c' P + a) dout + s') Q + b'
+      q = (int)(t % Q);
+      t /= Q;
+      sp = (int)(t % dout);
+      t /= dout;
+      p = (int)(t % P);
+      co = (int)(t / P);
+    } else {  // idx = ((c dout + s') P + a') Q + b
+      q = (int)(t % Q);
+      t /= Q;
+      p = (int)(t % P);
+      t /= P;
+      sp = (int)(t % dout);
+      co = (int)(t / dout);
+    }
+    T acc = Scalar<T>::zero();
+    for (int ci = 0; ci < Din; ++ci)
+      for (int s = 0; s < din; ++s) {
+        const int c = LEFT ? ci : co, cp = LEFT ? co : ci;
+        const T wv = w[((c * dout + sp) * din + s) * Dr + cp];
+        const T xv = LEFT ? X[(((long long)ci * P + p) * din + s) * Q + q] : X[(((long long)ci * P + p) * Q + q) * din + s];
+        acc = add(acc, mul(wv, xv));
+      }
+    Y[idx] = acc;
+  }
+}
+
+// update_left_op_environment / update_right_op_environment (environments.hpp:42-83) on device
+// buffers.  dims = {Dl, dout, din, Dr, bra_l, bra_r, ket_l, ket_r}; env / out are stacked
+// matrices E[c](a, b) as [c][a][b] (left: env over Dl with a, b = bra_l, ket_l; out over Dr with
+// bra_r, ket_r.  right: env over Dr with bra_r, ket_r; out over Dl with bra_l, ket_l).
+template <typename T>
+void openv_update(ttg_ctx* ctx, bool left, const int* dm, const void* env, const void* bra, const void* op,
+                  const void* ket, void* out) {
+  const int Dl = dm[0], dout = dm[1], din = dm[2], Dr = dm[3], al = dm[4], ar = dm[5], bl = dm[6], br = dm[7];
+  cudaStream_t st = ctx->stream;
+  const size_t es = sizeof(T);
+  const double fm = Scalar<T>::is_complex ? 8.0 : 2.0;
+  const size_t smem = (size_t)Dl * dout * din * Dr * es;
+  if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "op environment: MPO site too large"};
+  if (left) {
+    // X[c][a][s][b'] = E[c](a, b) B[b, s, b']: (Dl al) x bl times bl x (din br)
+    DevBuf X((size_t)Dl * al * din * br * es, st), Y((size_t)Dr * al * dout * br * es, st);
+    GemmParams g1{env, ket, X.p, 0, 0, 0, dconst(Dl * al), dconst(din * br), dconst(bl), nullptr, 0, nullptr, 1.0, 0};
+    {
+      ProfScope ps(ctx, TTG_PROF_GEMM, fm * Dl * al * (double)din * br * bl);
+      CK(gemm<T>(g1, OP_N, OP_N, Dl * al, din * br, 1, st, bl));
+    }
+    const long long tot = (long long)Dr * al * dout * br;
+    openv_mix_kernel<T, true><<<(int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256)), 256,
+                                smem, st>>>(static_cast<const T*>(X.p), static_cast<const T*>(op), Y.as<T>(), Dl, dout,
+                                            din, Dr, al, br);
+    CK(cudaGetLastError());
+    // out[c'] = A^H (ar x (al dout)) Y[c'] ((al dout) x br), batched over c'
+    GemmParams g3{bra, Y.p, out, 0, (long long)al * dout * br, (long long)ar * br, dconst(ar), dconst(br),
+                  dconst(al * dout), nullptr, 0, nullptr, 1.0, 0};
+    ProfScope ps(ctx, TTG_PROF_GEMM, fm * Dr * (double)ar * br * al * dout);
+    CK(gemm<T>(g3, OP_C, OP_N, ar, br, Dr, st, al * dout));
+  } else {
+    // Z[c'][a'][b][s] = E[c'](a', b') B[b, s, b']: (Dr ar) x br times (bl din x br)^T
+    DevBuf Z((size_t)Dr * ar * bl * din * es, st), Y((size_t)Dl * dout * ar * bl * es, st);
+    GemmParams g1{env, ket, Z.p, 0, 0, 0, dconst(Dr * ar), dconst(bl * din), dconst(br), nullptr, 0, nullptr, 1.0, 0};
+    {
+      ProfScope ps(ctx, TTG_PROF_GEMM, fm * Dr * ar * (double)bl * din * br);
+      CK(gemm<T>(g1, OP_N, OP_T, Dr * ar, bl * din, 1, st, br));
+    }
+    const long long tot = (long long)Dl * dout * ar * bl;
+    openv_mix_kernel<T, false><<<(int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256)), 256,
+                                 smem, st>>>(static_cast<const T*>(Z.p), static_cast<const T*>(op), Y.as<T>(), Dl, dout,
+                                             din, Dr, ar, bl);
+    CK(cudaGetLastError());
+    // out[c] = conj(A) (al x (dout ar)) Y[c] ((dout ar) x bl), batched over c
+    GemmParams g3{bra, Y.p, out, 0, (long long)dout * ar * bl, (long long)al * bl, dconst(al), dconst(bl),
+                  dconst(dout * ar), nullptr, 0, nullptr, 1.0, 0};
+    ProfScope ps(ctx, TTG_PROF_GEMM, fm * Dl * (double)al * bl * dout * ar);
+    CK(gemm<T>(g3, OP_R, OP_N, al, bl, Dl, st, dout * ar));
+  }
+  ctx->launches += 3;
+}
 }  // namespace
 }  // namespace ttg
+
+ttg_status ttg_apply_effective_two_site_dev(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
+                                            const void* W2, const void* R, const void* x, void* y) {
+  return guarded(ctx, [&] {
+    if (!dims || !L || !W1 || !W2 || !R || !x || !y) throw Error{TTG_INVALID, "null argument"};
+    for (int i = 0; i < 11; ++i)
+      if (dims[i] <= 0) throw Error{TTG_SHAPE, "apply_effective_two_site: bad dimension"};
+    CK(cudaSetDevice(ctx->device));
+    if (dtype == TTG_C128)
+      ttg::heff_two_site_dev<ttg::cplx>(ctx, dims, L, W1, W2, R, x, y);
+    else if (dtype == TTG_F64)
+      ttg::heff_two_site_dev<double>(ctx, dims, L, W1, W2, R, x, y);
+    else
+      throw Error{TTG_INVALID, "apply_effective_two_site: dtype"};
+  });
+}
+
+ttg_status ttg_op_env_update(ttg_ctx* ctx, int dtype, int side, const int* dims, const void* env, const void* bra,
+                             const void* op, const void* ket, void* out) {
+  return guarded(ctx, [&] {
+    if (!dims || !env || !bra || !op || !ket || !out) throw Error{TTG_INVALID, "null argument"};
+    for (int i = 0; i < 8; ++i)
+      if (dims[i] <= 0) throw Error{TTG_SHAPE, "op environment: bad dimension"};
+    if (side != TTG_LEFT_TO_RIGHT && side != TTG_RIGHT_TO_LEFT) throw Error{TTG_INVALID, "op environment: side"};
+    CK(cudaSetDevice(ctx->device));
+    const bool left = side == TTG_LEFT_TO_RIGHT;
+    if (dtype == TTG_C128)
+      ttg::openv_update<ttg::cplx>(ctx, left, dims, env, bra, op, ket, out);
+    else if (dtype == TTG_F64)
+      ttg::openv_update<double>(ctx, left, dims, env, bra, op, ket, out);
+    else
+      throw Error{TTG_INVALID, "op environment: dtype"};
+  });
+}
 
 ttg_status ttg_apply_effective_two_site(ttg_ctx* ctx, int dtype, const int* dims, const void* L, const void* W1,
                                         const void* W2, const void* R, const void* x, void* y) {

@@ -1435,7 +1435,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   // 384 x 192 exact-pass QRs measured 1.5 ms per call faster without it.  Complex: C3 3.36 -> 2.57 s
   // once t_combine keeps T_O in shared memory; the rank-32 updates stream the trailing matrix
   // from HBM four times as often)
-  const bool two_level = two_level_env >= 0 ? two_level_env != 0 : k >= 512;
+  const bool two_level = w.keep_wy ? true : (two_level_env >= 0 ? two_level_env != 0 : qr_two_level(m, n));
   const int nblk_in = (k + QR_NB - 1) / QR_NB;
   T* To_all = Tt + (size_t)nblk_in * QR_NB * QR_NB;  // outer WY factors, QR_NBO x QR_NBO each
   T* Sbuf = To_all + (size_t)((k + QR_NBO - 1) / QR_NBO) * QR_NBO * QR_NBO;
@@ -1601,7 +1601,7 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
       if ((e = gemm<T>(g3, OP_N, OP_N, mp, nt, chains, s)) != cudaSuccess) return e;
       nl += 3;
     }
-    if (two_level && j0 + jb == jend && (jend < n || p.Q))
+    if (two_level && j0 + jb == jend && (jend < n || p.Q || w.keep_wy))
       if ((e = outer(J0, jend, jend < n)) != cudaSuccess) return e;
   }
   if (coop_part) cudaFreeAsync(coop_part, s);
@@ -1645,6 +1645,52 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   if (launches) *launches += nl;
   return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t householder_apply_q(const void* Vv, const void* Tw, int m, int k, void* Xv, int r, void* W1, void* W2,
+                                cudaStream_t s, long long* launches) {
+  if (m <= 0 || k <= 0 || r <= 0) return cudaSuccess;
+  const T* V = static_cast<const T*>(Vv);
+  T* X = static_cast<T*>(Xv);
+  const int nblk_in = (k + QR_NB - 1) / QR_NB;
+  const T* To_all = static_cast<const T*>(Tw) + (size_t)nblk_in * QR_NB * QR_NB;
+  const int nblk = (k + QR_NBO - 1) / QR_NBO;
+  cudaError_t e;
+  long long nl = 0;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * QR_NBO;
+    const int jb = (k - j0) < QR_NBO ? (k - j0) : QR_NBO;
+    const int mp = m - j0;
+    // W1 = V_b^H X[j0:, :] (jb x r)
+    GemmParams g1{V + (size_t)j0 * k + j0, X + (size_t)j0 * r, W1, 0, 0, 0, dconst(jb), dconst(r), dconst(mp), nullptr,
+                  0, nullptr, 1.0, 0};
+    g1.lda = k;
+    g1.ldb = r;
+    g1.ldc = r;
+    if ((e = gemm<T>(g1, OP_C, OP_N, jb, r, 1, s, mp)) != cudaSuccess) return e;
+    // W2 = T_b W1
+    GemmParams g2{To_all + (size_t)b * QR_NBO * QR_NBO, W1, W2, 0, 0, 0, dconst(jb), dconst(r), dconst(jb), nullptr, 0,
+                  nullptr, 1.0, 0};
+    g2.lda = QR_NBO;
+    g2.ldb = r;
+    g2.ldc = r;
+    if ((e = gemm<T>(g2, OP_N, OP_N, jb, r, 1, s)) != cudaSuccess) return e;
+    // X[j0:, :] -= V_b W2
+    GemmParams g3{V + (size_t)j0 * k + j0, W2, X + (size_t)j0 * r, 0, 0, 0, dconst(mp), dconst(r), dconst(jb), nullptr,
+                  0, nullptr, -1.0, 1};
+    g3.lda = k;
+    g3.ldb = r;
+    g3.ldc = r;
+    if ((e = gemm<T>(g3, OP_N, OP_N, mp, r, 1, s)) != cudaSuccess) return e;
+    nl += 3;
+  }
+  if (launches) *launches += nl;
+  return cudaGetLastError();
+}
+template cudaError_t householder_apply_q<double>(const void*, const void*, int, int, void*, int, void*, void*,
+                                                 cudaStream_t, long long*);
+template cudaError_t householder_apply_q<cplx>(const void*, const void*, int, int, void*, int, void*, void*,
+                                               cudaStream_t, long long*);
 
 template <typename T>
 cudaError_t conj_transpose(const void* src, long long s_src, int rows, int cols, void* dst, long long s_dst, int chains,

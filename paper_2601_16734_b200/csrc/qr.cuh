@@ -73,6 +73,7 @@ struct QrBlockedWork {
   void* W2;  // 128 x n
   void* P;   // panel scratch m x 32 (global fallback of the panel kernel)
   long long sA, sV, sT, sW, sP;  // per-chain strides
+  int keep_wy = 0;  // R only, but complete every outer WY factor so V / T can apply Q later
 };
 constexpr int QR_NB = 32;
 constexpr int QR_NBO = 128;  // outer block: trailing and Q updates use K = 128 (two-level blocking)
@@ -85,5 +86,14 @@ cudaError_t conj_transpose(const void* src, long long s_src, int rows, int cols,
 template <typename T>
 cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, int chains, cudaStream_t s,
                                    long long* launches);
+// Two-level blocking is used for k = min(m, n) >= 512 (the only case householder_apply_q supports).
+inline bool qr_two_level(int m, int n) { return (m < n ? m : n) >= 512; }
+// X (m x r, row-major, ld r) <- Q X for the thin Q (m x k) of a two-level blocked QR run with
+// keep_wy (V: m x k reflectors with ld k, Tw: its T workspace), i.e. Q M = H_1 .. H_k [M; 0]
+// when X holds M (k x r) on top of zeros: the backward Q formation applied to X instead of the
+// identity, 4 m k r flops instead of forming Q (about 2 m k^2) and multiplying.  W1, W2: 128 x r.
+template <typename T>
+cudaError_t householder_apply_q(const void* V, const void* Tw, int m, int k, void* X, int r, void* W1, void* W2,
+                                cudaStream_t s, long long* launches);
 
 }  // namespace ttg
