@@ -44,7 +44,8 @@ ctx = t.context()
 dims = (C.c_int * 11)(D, D, D, 2, 2, 2, 2, chi, chi, chi, chi)
 dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (L, w1, w2, R, x)]
 yd = torch.empty(chi * 4 * chi, dtype=torch.float64, device="cuda")
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()  # a real stream shared by the library and the events (0 = the library's own)
+torch.cuda.set_stream(stream)
 ctx.set_stream(stream.cuda_stream)
 args = [C.c_void_p(a.data_ptr()) for a in dev] + [C.c_void_p(yd.data_ptr())]
 for _ in range(3):
