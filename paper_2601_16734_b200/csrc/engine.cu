@@ -2109,39 +2109,52 @@ ttg_status ttg_mpo_save(ttg_ctx* ctx, const ttg_dmpo* w, const char* path) {
 // ---------------------------------------------------------------------------
 namespace ttg {
 namespace {
+// Both MPO sites at once: V[a'][s1'][s2'][c2][B] = sum_{c0,s1,s2} W12[c0,s1',s1,s2',s2,c2] XL[c0][a'][s1][s2][B]
+// with W12 = sum_{c1} W1[c0,s1',s1,c1] W2[c1,s2',s2,c2] formed once per CTA in shared memory.  One thread
+// per (a', B) reads its D0 d1 d2 values of XL once (coalesced over B) and writes all d1o d2o D2 outputs,
+// so XL is read once and V written once (memory-bound).
 template <typename T>
 __global__ void heff_mix_kernel(const T* XL, const T* W1, const T* W2, T* V, int D0, int D1, int D2, int d1o, int d1,
                                 int d2o, int d2, int chiAo, int chiB) {
   extern __shared__ __align__(16) unsigned char heff_smem[];
-  T* w1 = reinterpret_cast<T*>(heff_smem);
-  T* w2 = w1 + D0 * d1o * d1 * D1;
-  for (int i = threadIdx.x; i < D0 * d1o * d1 * D1; i += blockDim.x) w1[i] = W1[i];
-  for (int i = threadIdx.x; i < D1 * d2o * d2 * D2; i += blockDim.x) w2[i] = W2[i];
+  T* w12 = reinterpret_cast<T*>(heff_smem);  // [c0][s1o][s1][s2o][s2][c2]
+  const int n12 = D0 * d1o * d1 * d2o * d2 * D2;
+  for (int i = threadIdx.x; i < n12; i += blockDim.x) {
+    int t = i;
+    const int c2 = t % D2;
+    t /= D2;
+    const int s2 = t % d2;
+    t /= d2;
+    const int s2o = t % d2o;
+    t /= d2o;
+    const int s1 = t % d1;
+    t /= d1;
+    const int s1o = t % d1o;
+    const int c0 = t / d1o;
+    T acc = Scalar<T>::zero();
+    for (int c1 = 0; c1 < D1; ++c1)
+      acc = add(acc, mul(W1[((c0 * d1o + s1o) * d1 + s1) * D1 + c1], W2[((c1 * d2o + s2o) * d2 + s2) * D2 + c2]));
+    w12[i] = acc;
+  }
   __syncthreads();
-  // V[a'][s1'][s2'][c2][B]; XL[c0][a'][s1][s2][B]
-  const long long total = (long long)chiAo * d1o * d2o * D2 * chiB;
+  const int nin = D0 * d1 * d2;
+  const long long total = (long long)chiAo * chiB;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    long long t = idx;
-    const int B = (int)(t % chiB);
-    t /= chiB;
-    const int c2 = (int)(t % D2);
-    t /= D2;
-    const int s2o = (int)(t % d2o);
-    t /= d2o;
-    const int s1o = (int)(t % d1o);
-    const int a = (int)(t / d1o);
-    T acc = Scalar<T>::zero();
-    for (int c0 = 0; c0 < D0; ++c0)
-      for (int s1 = 0; s1 < d1; ++s1)
-        for (int s2 = 0; s2 < d2; ++s2) {
-          T w = Scalar<T>::zero();
-          for (int c1 = 0; c1 < D1; ++c1)
-            w = add(w, mul(w1[((c0 * d1o + s1o) * d1 + s1) * D1 + c1], w2[((c1 * d2o + s2o) * d2 + s2) * D2 + c2]));
-          const T x = XL[((((size_t)c0 * chiAo + a) * d1 + s1) * d2 + s2) * chiB + B];
-          acc = add(acc, mul(w, x));
+    const int B = (int)(idx % chiB), a = (int)(idx / chiB);
+    for (int s1o = 0; s1o < d1o; ++s1o)
+      for (int s2o = 0; s2o < d2o; ++s2o)
+        for (int c2 = 0; c2 < D2; ++c2) {
+          T acc = Scalar<T>::zero();
+          for (int c0 = 0; c0 < D0; ++c0)
+            for (int s1 = 0; s1 < d1; ++s1)
+              for (int s2 = 0; s2 < d2; ++s2) {
+                const T x = XL[((((size_t)c0 * chiAo + a) * d1 + s1) * d2 + s2) * chiB + B];
+                acc = add(acc, mul(w12[((((c0 * d1o + s1o) * d1 + s1) * d2o + s2o) * d2 + s2) * D2 + c2], x));
+              }
+          V[((((size_t)a * d1o + s1o) * d2o + s2o) * D2 + c2) * chiB + B] = acc;
         }
-    V[idx] = acc;
+    (void)nin;
   }
 }
 
@@ -2163,9 +2176,11 @@ void heff_two_site_dev(ttg_ctx* ctx, const int* dm, const void* L, const void* W
     ProfScope ps(ctx, TTG_PROF_GEMM, (Scalar<T>::is_complex ? 8.0 : 2.0) * M1 * (double)N1 * chiA);
     CK(gemm<T>(g1, OP_N, OP_N, M1, N1, 1, st, chiA));
   }
-  const size_t smem = (nW1 + nW2) * es;
+  const size_t smem = (size_t)D0 * d1o * d1 * d2o * d2 * D2 * es;  // fused W12
   if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
-  const long long tot = (long long)nV;
+  (void)nW1;
+  (void)nW2;
+  const long long tot = (long long)chiAo * chiB;
   const int blocks = (int)std::max<long long>(1, std::min<long long>(148 * 8, (tot + 255) / 256));
   {
     ProfScope ps(ctx, TTG_PROF_EXPAND);
