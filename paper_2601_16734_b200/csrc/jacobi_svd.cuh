@@ -70,6 +70,14 @@ bool jacobi_grid_eligible(int lmax, int kmax, int chains, size_t es);
 template <typename T>
 cudaError_t jacobi_svd_grid(const SvdParams& p, int lmax, int kmax, int chains, void* work, cudaStream_t s);
 
+
+// Block-Gram variant for one large real split (jacobi_bg.cu): a cluster per block pair keeps the
+// pair's rows in shared memory, rotates the pair's Gram matrix and applies the accumulated
+// rotations by DMMA.  Same workspace as jacobi_svd_grid.  cudaErrorNotSupported when the
+// cooperative cluster launch is not available (the caller falls back to the grid kernels).
+bool jacobi_bg_eligible(int lmax, int kmax, int chains, size_t es);
+cudaError_t jacobi_svd_bg(const SvdParams& p, int lmax, int kmax, void* work, cudaStream_t s);
+
 }  // namespace ttg
 
 namespace ttg {

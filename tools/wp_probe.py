@@ -42,7 +42,7 @@ def c4_like(m, n, cplx=False):
 
 
 tag = os.environ.get("TTG_SVD_WP", "8")
-for (m, n, cplx) in [(1024, 1024, False), (512, 1024, False), (256, 256, True), (256, 512, True)]:
+for (m, n, cplx) in ([] if __name__ != "__main__" else [(1024, 1024, False), (512, 1024, False), (256, 256, True), (256, 512, True)]):
     A = c4_like(m, n, cplx)
     L = np.linalg.qr(np.linalg.qr(A)[1].conj().T)[1].conj().T  # Drmac-Veselic preconditioned matrix
     run(L, 0)
