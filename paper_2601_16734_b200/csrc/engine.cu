@@ -248,14 +248,18 @@ struct Engine {
   bool chain_on(int c, bool check_active) const { return !(check_active && d_state) || hs[c].active; }
 
   void G(const void* A, long long sA, const void* Bm, long long sB, void* C, long long sC, DimExpr M, DimExpr N,
-         DimExpr K, int opA, int opB, bool check_active, int beta = 0) {
+         DimExpr K, int opA, int opB, bool check_active, int beta = 0, bool a_upper = false) {
     double flops = 0.0;
     if (live_dims(check_active))
       for (int c = 0; c < B; ++c)
-        if (chain_on(c, check_active))
-          flops += (Scalar<T>::is_complex ? 8.0 : 2.0) * M.eval(hb.data(), c, ld) * (double)N.eval(hb.data(), c, ld) *
-                   K.eval(hb.data(), c, ld);
+        if (chain_on(c, check_active)) {
+          const double m = M.eval(hb.data(), c, ld), kk = K.eval(hb.data(), c, ld);
+          // upper triangular / trapezoidal A: row i multiplies k >= i only
+          const double mk = a_upper ? (m <= kk ? m * kk - m * (m - 1) / 2.0 : kk * (kk + 1) / 2.0) : m * kk;
+          flops += (Scalar<T>::is_complex ? 8.0 : 2.0) * mk * (double)N.eval(hb.data(), c, ld);
+        }
     GemmParams p{A, Bm, C, sA, sB, sC, M, N, K, d_bonds, ld, check_active ? d_state : nullptr, 1.0, beta};
+    p.a_upper = a_upper ? 1 : 0;
     ProfScope ps(ctx, TTG_PROF_GEMM, flops);
     CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st, ub(K)));
     ++ctx->launches;
@@ -751,7 +755,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     // carried = R * next.right_matrix()  (mps.hpp:202)
     const int nxt = (k == 0 && curp != cbuf[0]) ? 0 : cur ^ 1;
     E.G(Rb.p, sR, guess.site[k + 1], guess.cap[k + 1], cbuf[nxt], sC, dconst(q[k + 1]), dconst(d[k + 1] * g[k + 2]),
-        dconst(g[k + 1]), OP_N, OP_N, false);
+        dconst(g[k + 1]), OP_N, OP_N, false, 0, true);  // R is upper triangular: half the product
     cur = nxt;
     curp = cbuf[cur];
     s_cur = sC;

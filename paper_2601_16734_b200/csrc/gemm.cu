@@ -139,8 +139,10 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
   const int ktiles_all = (K + BK - 1) / BK;
   const int splits = gridDim.z;
   const int per = (ktiles_all + splits - 1) / splits;
-  const int kt0 = blockIdx.z * per;
+  int kt0 = blockIdx.z * per;
   const int kt1 = min(ktiles_all, kt0 + per);
+  if constexpr (OPA == OP_N || OPA == OP_R)
+    if (p.a_upper) kt0 = max(kt0, m0 / BK);
   const int ktiles = max(0, kt1 - kt0);
   if (ktiles > 0) load_tile(0, kt0 * BK);
   cp_commit();

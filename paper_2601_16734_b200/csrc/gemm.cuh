@@ -29,6 +29,9 @@ struct GemmParams {
   // split-K partial tiles (set by gemm(): [chain][split][mmax][nmax], reduced in fixed order)
   void* ws = nullptr;
   int ws_m = 0, ws_n = 0;
+  // 1: op(A) = A (OP_N / OP_R) is upper triangular or trapezoidal (A[i][k] = 0 for k < i), e.g. the R
+  // factor carried into the next site (mps.hpp:202): output row tiles skip the k range left of the diagonal
+  int a_upper = 0;
 };
 
 // Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only);
