@@ -497,7 +497,15 @@ void Engine<T>::split_large(const void* theta, long long s_theta, DimExpr M, Dim
       qr_blocked_elems<T>(qr_rows, qr_cols, &a, &v, &t2, &w2, &pp);
       DevBuf wa(a * es, st), wv(v * es, st), wt(t2 * es, st), w1b(w2 * es, st), w2b(w2 * es, st), wp(pp * es, st);
       QrParams qp{Mb.p, 0, nullptr, 0, R.p, 0, nullptr, 0, qr_rows, qr_cols};
-      const QrBlockedWork qw{wa.p, wv.p, wt.p, w1b.p, w2b.p, wp.p, 0, 0, 0, 0, 0};
+      QrBlockedWork qw{wa.p, wv.p, wt.p, w1b.p, w2b.p, wp.p, 0, 0, 0, 0, 0};
+      // R-only QR of a matrix with few rows: the outer WY factor (S product + t_combine per 128 columns)
+      // costs more than the rank-128 updates save (C4 A/B: 1024 x 1024 splits 50 ms per call faster with
+      // rank-32 updates, 4096 x 1024 truncating-pass splits another 7 ms).  TTG_QR_PRE2L: two-level from this many rows on.
+      static const int pre2l = [] {
+        const char* e = getenv("TTG_QR_PRE2L");
+        return e ? atoi(e) : (1 << 30);
+      }();
+      qw.two_level = qr_rows >= pre2l ? -1 : 0;
       long long nl = 0;
       const double big = std::max(qr_rows, qr_cols), sm = std::min(qr_rows, qr_cols);
       ProfScope ps(ctx, TTG_PROF_QR, (Scalar<T>::is_complex ? 4.0 : 1.0) * 2.0 * sm * sm * (big - sm / 3.0));

@@ -1435,7 +1435,10 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
   // 384 x 192 exact-pass QRs measured 1.5 ms per call faster without it.  Complex: C3 3.36 -> 2.57 s
   // once t_combine keeps T_O in shared memory; the rank-32 updates stream the trailing matrix
   // from HBM four times as often)
-  const bool two_level = w.keep_wy ? true : (two_level_env >= 0 ? two_level_env != 0 : qr_two_level(m, n));
+  const bool two_level = w.keep_wy ? true
+                         : two_level_env >= 0 ? two_level_env != 0
+                         : w.two_level >= 0 ? w.two_level != 0
+                                            : qr_two_level(m, n);
   const int nblk_in = (k + QR_NB - 1) / QR_NB;
   T* To_all = Tt + (size_t)nblk_in * QR_NB * QR_NB;  // outer WY factors, QR_NBO x QR_NBO each
   T* Sbuf = To_all + (size_t)((k + QR_NBO - 1) / QR_NBO) * QR_NBO * QR_NBO;

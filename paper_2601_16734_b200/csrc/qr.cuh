@@ -74,6 +74,7 @@ struct QrBlockedWork {
   void* P;   // panel scratch m x 32 (global fallback of the panel kernel)
   long long sA, sV, sT, sW, sP;  // per-chain strides
   int keep_wy = 0;  // R only, but complete every outer WY factor so V / T can apply Q later
+  int two_level = -1;  // -1: by shape (qr_two_level); 0 / 1: force 32-column / 128-column trailing updates
 };
 constexpr int QR_NB = 32;
 constexpr int QR_NBO = 128;  // outer block: trailing and Q updates use K = 128 (two-level blocking)
