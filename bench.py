@@ -273,7 +273,9 @@ def _workload_desc(cfg):
 # ncu --clock-control none, profiles/r01_dram_svd.txt): the split matrices stay L2-resident, so
 # traffic is about one read of the matrix per launch
 _SVD_TRAFFIC = {"C2": {"kernel": "jacobi_cluster_kernel<double,16,8,128,2>", "bytes": 204117},
-                "C4": {"kernel": "jacobi_grid_kernel<double,4,4,256,1>", "bytes": 9784448}}
+                # round 2: block-Gram Jacobi on a 1024 x 1024 split (profiles/r02_jbg_c4.raw.csv: 8.46 MB read +
+                # 2.26 MB written for the 8 MiB matrix, 16.98 ms)
+                "C4": {"kernel": "jacobi_bg_kernel<16,256>", "bytes": 10720256}}
 
 
 def _roofline(prof, cfg_name=None):
@@ -284,8 +286,10 @@ def _roofline(prof, cfg_name=None):
     achieved = p["flops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
     return {
         "bound": "fp64",
-        "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)", "svd": "ttg::jacobi_svd_kernel",
-                   "qr": "ttg::qr_kernel"}[dom],
+        "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)",
+                   "svd": "ttg::" + (_SVD_TRAFFIC[cfg_name]["kernel"] if cfg_name in _SVD_TRAFFIC
+                                     else "jacobi_svd_kernel"),
+                   "qr": "ttg::qr_panel_cl_kernel + DMMA updates"}[dom],
         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
         "traffic": (_SVD_TRAFFIC[cfg_name]["bytes"] if dom == "svd" and cfg_name in _SVD_TRAFFIC else None),

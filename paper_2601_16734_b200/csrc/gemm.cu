@@ -6,6 +6,8 @@
 #include "gemm.cuh"
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 namespace ttg {
 namespace {
@@ -35,8 +37,246 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// Grouped raster: consecutive CTAs walk RASTER_G tile rows of one tile column before moving to the
+// next column, so a B tile column (K x 64) is reused from L2 by the group's rows and the group's A
+// rows stay resident while the columns stream (row-major order re-read all of B once per tile row:
+// 3.33 GB of DRAM reads for the 0.37 GB operands of the C4 product Y = X T, profiles/r01_gemm_c4Y).
+__device__ __forceinline__ void tile_of(int bid, int tiles_m, int tiles_n, int RASTER_G, int& tm, int& tn) {
+  if (RASTER_G <= 1) {  // row-major
+    tm = bid / tiles_n;
+    tn = bid - tm * tiles_n;
+    return;
+  }
+  const int gsz = RASTER_G * tiles_n;
+  const int g = bid / gsz, r = bid - g * gsz;
+  const int first = g * RASTER_G;
+  const int gm = min(RASTER_G, tiles_m - first);
+  tn = r / gm;
+  tm = first + (r - tn * gm);
+}
+
+// ---- TMA (bulk asynchronous copy) + mbarrier helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "TTG_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra TTG_DONE;\n"
+      "bra TTG_WAIT;\n"
+      "TTG_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one contiguous row segment global -> shared through the TMA engine (SASS UBLKCP); completion is
+// counted in bytes on the stage's mbarrier
+__device__ __forceinline__ void tma_row(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+constexpr int TMA_STAGES = 4;
+
+// TMA-staged variant of gemm_kernel for products whose shapes are known on the host and satisfy
+// gemm_tma_ok(): same 64 x 64 x BK tiles, warp layout and padded (bank-conflict free) shared-memory
+// layouts, but the operand rows of a stage are moved by bulk asynchronous copies (one per tile row,
+// 128 B .. 1 KB each, issued by the lanes of warp 0) that complete on the stage's mbarrier, four
+// stages deep.  No ragged K (K % BK == 0); rows / columns beyond M / N are never copied and their
+// (garbage) products are discarded by the epilogue's bounds check.
 template <typename T, int OPA, int OPB>
-__global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_n) {
+__global__ void __launch_bounds__(NTHREADS) gemm_tma_kernel(GemmParams p, int tiles_m, int tiles_n) {
+  constexpr int PAD = Pad<T>::value;
+  constexpr int BK = Depth<T>::value;
+  constexpr int SA = BM + PAD, SB = BN + PAD;
+  constexpr bool CPX = Scalar<T>::is_complex;
+  constexpr bool AK = (OPA == OP_N || OPA == OP_R);
+  constexpr bool BK_ = (OPB == OP_T || OPB == OP_C);
+  constexpr int SK = BK + 4;
+  constexpr int A_ELEMS = AK ? BM * SK : BK * SA;
+  constexpr int B_ELEMS = BK_ ? BN * SK : BK * SB;
+  extern __shared__ __align__(16) unsigned char tma_smem[];
+  T* const As = reinterpret_cast<T*>(tma_smem);
+  T* const Bs = As + TMA_STAGES * A_ELEMS;
+  __shared__ __align__(8) unsigned long long full[TMA_STAGES];
+  auto a_at = [&](int st, int k, int m) -> T& { return AK ? As[st * A_ELEMS + m * SK + k] : As[st * A_ELEMS + k * SA + m]; };
+  auto b_at = [&](int st, int k, int n) -> T& { return BK_ ? Bs[st * B_ELEMS + n * SK + k] : Bs[st * B_ELEMS + k * SB + n]; };
+
+  const int chain = blockIdx.y;
+  if (p.st && !p.st[chain].active) return;
+  const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
+  const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
+  const int K = p.K.eval(p.bonds, chain, p.bonds_ld);
+  int tm, tn;
+  tile_of(blockIdx.x, tiles_m, tiles_n, p.raster, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= M || n0 >= N) return;
+
+  const long long lda = p.lda ? p.lda : (AK ? K : M);
+  const long long ldb = p.ldb ? p.ldb : (BK_ ? K : N);
+  const long long ldc = p.ldc ? p.ldc : N;
+  const T* A = static_cast<const T*>(p.A) + p.sA * chain;
+  const T* B = static_cast<const T*>(p.B) + p.sB * chain;
+  T* C = static_cast<T*>(p.C) + p.sC * chain;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int mrows = min(BM, M - m0), ncols = min(BN, N - n0);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < TMA_STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  double acc[2][4][4];
+  double acci[CPX ? 2 : 1][CPX ? 4 : 1][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+  if constexpr (CPX) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acci[i][j][r] = 0.0;
+  }
+
+  // warp 0: expected bytes of the stage, then one bulk copy per operand row
+  const unsigned a_bytes = (AK ? (unsigned)mrows * BK : (unsigned)BK * mrows) * (unsigned)sizeof(T);
+  const unsigned b_bytes = (BK_ ? (unsigned)ncols * BK : (unsigned)BK * ncols) * (unsigned)sizeof(T);
+  auto issue = [&](int stage, int k0) {
+    if (lane == 0) mbar_expect_tx(&full[stage], a_bytes + b_bytes);
+    __syncwarp();
+    if constexpr (AK) {
+      for (int m = lane; m < mrows; m += 32)
+        tma_row(&a_at(stage, 0, m), A + (m0 + m) * lda + k0, BK * sizeof(T), &full[stage]);
+    } else {
+      for (int k = lane; k < BK; k += 32)
+        tma_row(&a_at(stage, k, 0), A + (k0 + k) * lda + m0, mrows * sizeof(T), &full[stage]);
+    }
+    if constexpr (BK_) {
+      for (int n = lane; n < ncols; n += 32)
+        tma_row(&b_at(stage, 0, n), B + (n0 + n) * ldb + k0, BK * sizeof(T), &full[stage]);
+    } else {
+      for (int k = lane; k < BK; k += 32)
+        tma_row(&b_at(stage, k, 0), B + (k0 + k) * ldb + n0, ncols * sizeof(T), &full[stage]);
+    }
+  };
+
+  const int ktiles_all = K / BK;
+  const int splits = gridDim.z;
+  const int per = (ktiles_all + splits - 1) / splits;
+  int kt0 = blockIdx.z * per;
+  const int kt1 = min(ktiles_all, kt0 + per);
+  if constexpr (AK)
+    if (p.a_upper) kt0 = max(kt0, m0 / BK);
+  const int ktiles = max(0, kt1 - kt0);
+  if (warp == 0)
+    for (int s = 0; s < TMA_STAGES - 1 && s < ktiles; ++s) issue(s, (kt0 + s) * BK);
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int stage = kt % TMA_STAGES;
+    // the stage of tile kt + STAGES - 1 was read in iteration kt - 1 (all warps are past its barrier)
+    if (warp == 0 && kt + TMA_STAGES - 1 < ktiles) issue((kt + TMA_STAGES - 1) % TMA_STAGES, (kt0 + kt + TMA_STAGES - 1) * BK);
+    mbar_wait(&full[stage], (kt / TMA_STAGES) & 1);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      if constexpr (!CPX) {
+        double a[2][2], b[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          a[i][0] = a_at(stage, kk + t4, wm + i * 16 + g);
+          a[i][1] = a_at(stage, kk + t4, wm + i * 16 + g + 8);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = b_at(stage, kk + t4, wn + j * 8 + g);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i][0], a[i][1], b[j]);
+      } else {
+        constexpr double sa = (OPA == OP_C || OPA == OP_R) ? -1.0 : 1.0;
+        constexpr double sb = (OPB == OP_C || OPB == OP_R) ? -1.0 : 1.0;
+        double ar[2][2], ai[2][2], nai[2][2], br[4], bi[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const cplx x0 = a_at(stage, kk + t4, wm + i * 16 + g);
+          const cplx x1 = a_at(stage, kk + t4, wm + i * 16 + g + 8);
+          ar[i][0] = x0.x; ai[i][0] = sa * x0.y; nai[i][0] = -ai[i][0];
+          ar[i][1] = x1.x; ai[i][1] = sa * x1.y; nai[i][1] = -ai[i][1];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const cplx y = b_at(stage, kk + t4, wn + j * 8 + g);
+          br[j] = y.x; bi[j] = sb * y.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dmma(acc[i][j], ar[i][0], ar[i][1], br[j]);
+            dmma(acc[i][j], nai[i][0], nai[i][1], bi[j]);
+            dmma(acci[i][j], ar[i][0], ar[i][1], bi[j]);
+            dmma(acci[i][j], ai[i][0], ai[i][1], br[j]);
+          }
+      }
+    }
+    __syncthreads();
+  }
+
+  const double alpha = p.alpha;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + wm + i * 16 + g + (r >= 2 ? 8 : 0);
+        const int n = n0 + wn + j * 8 + 2 * t4 + (r & 1);
+        if (m < M && n < N) {
+          T* dst = C + m * ldc + n;
+          if (splits > 1) {
+            T* w = static_cast<T*>(p.ws) + (((long long)chain * splits + blockIdx.z) * p.ws_m + m) * p.ws_n + n;
+            if constexpr (!CPX)
+              *w = alpha * acc[i][j][r];
+            else
+              *w = cplx{alpha * acc[i][j][r], alpha * acci[i][j][r]};
+          } else if constexpr (!CPX) {
+            const double v = alpha * acc[i][j][r];
+            *dst = p.beta ? *dst + v : v;
+          } else {
+            cplx v{alpha * acc[i][j][r], alpha * acci[i][j][r]};
+            if (p.beta) v = add(*dst, v);
+            *dst = v;
+          }
+        }
+      }
+}
+
+template <typename T, int OPA, int OPB>
+constexpr size_t gemm_tma_smem() {
+  constexpr int PAD = Pad<T>::value, BK = Depth<T>::value, SK = BK + 4;
+  constexpr bool AK = (OPA == OP_N || OPA == OP_R), BK_ = (OPB == OP_T || OPB == OP_C);
+  return (size_t)TMA_STAGES * ((AK ? BM * SK : BK * (BM + PAD)) + (BK_ ? BN * SK : BK * (BN + PAD))) * sizeof(T);
+}
+
+template <typename T, int OPA, int OPB>
+__global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_m, int tiles_n) {
   constexpr int PAD = Pad<T>::value;
   constexpr int BK = Depth<T>::value;
   constexpr int KSH = BK == 16 ? 4 : 3;
@@ -60,7 +300,8 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
   const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
   const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
   const int K = p.K.eval(p.bonds, chain, p.bonds_ld);
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  int tm, tn;
+  tile_of(blockIdx.x, tiles_m, tiles_n, p.raster, tm, tn);
   const int m0 = tm * BM, n0 = tn * BN;
   if (m0 >= M || n0 >= N) return;
 
@@ -247,15 +488,58 @@ __global__ void splitk_reduce_kernel(GemmParams p, int splits) {
   }
 }
 
-template <typename T, int OPA>
-cudaError_t launch_b(const GemmParams& p, int opB, dim3 grid, int tiles_n, cudaStream_t s) {
-  switch (opB) {
-    case OP_N: gemm_kernel<T, OPA, OP_N><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
-    case OP_T: gemm_kernel<T, OPA, OP_T><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
-    case OP_C: gemm_kernel<T, OPA, OP_C><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
-    default: gemm_kernel<T, OPA, OP_R><<<grid, NTHREADS, 0, s>>>(p, tiles_n); break;
+template <typename T, int OPA, int OPB>
+cudaError_t launch_one(const GemmParams& p, dim3 grid, int tiles_m, int tiles_n, bool tma, cudaStream_t s) {
+  if (tma) {
+    constexpr size_t smem = gemm_tma_smem<T, OPA, OPB>();
+    static const cudaError_t attr = cudaFuncSetAttribute(gemm_tma_kernel<T, OPA, OPB>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return attr;
+    gemm_tma_kernel<T, OPA, OPB><<<grid, NTHREADS, smem, s>>>(p, tiles_m, tiles_n);
+  } else {
+    gemm_kernel<T, OPA, OPB><<<grid, NTHREADS, 0, s>>>(p, tiles_m, tiles_n);
   }
   return cudaGetLastError();
+}
+
+template <typename T, int OPA>
+cudaError_t launch_b(const GemmParams& p, int opB, dim3 grid, int tiles_m, int tiles_n, bool tma, cudaStream_t s) {
+  switch (opB) {
+    case OP_N: return launch_one<T, OPA, OP_N>(p, grid, tiles_m, tiles_n, tma, s);
+    case OP_T: return launch_one<T, OPA, OP_T>(p, grid, tiles_m, tiles_n, tma, s);
+    case OP_C: return launch_one<T, OPA, OP_C>(p, grid, tiles_m, tiles_n, tma, s);
+    default: return launch_one<T, OPA, OP_R>(p, grid, tiles_m, tiles_n, tma, s);
+  }
+}
+
+// The TMA kernel needs host-known shapes (constant DimExpr), no ragged K, and 16-byte aligned,
+// 16-byte sized row segments: even leading dimensions / extents for f64 (complex elements are 16 B).
+template <typename T>
+bool gemm_tma_ok(const GemmParams& p, int opA, int opB) {
+  static const bool enabled = [] {
+    const char* e = getenv("TTG_GEMM_TMA");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || p.M.idx >= 0 || p.N.idx >= 0 || p.K.idx >= 0) return false;
+  const long long M = p.M.mult, N = p.N.mult, K = p.K.mult;
+  constexpr int BK = Depth<T>::value;
+  if (K < 2 * BK || K % BK != 0 || M * N < 64 * 64) return false;
+  const bool ak = (opA == OP_N || opA == OP_R), bk = (opB == OP_T || opB == OP_C);
+  // k-contiguous operands would be staged in 128-byte row copies (64 per stage): measured 2x slower
+  // than the cp.async kernel (17.9 vs 33.9 TF/s, 4096^3); m- / n-contiguous operands move in 512 B - 1 KB
+  // rows (16 + 16 copies per stage) and win (psi^H X: 27.5 vs 25.9 TF/s).  TTG_GEMM_TMA=2 forces all.
+  static const bool all_ops = [] {
+    const char* e = getenv("TTG_GEMM_TMA");
+    return e && e[0] == '2';
+  }();
+  if ((ak || bk) && !all_ops) return false;
+  const long long lda = p.lda ? p.lda : (ak ? K : M), ldb = p.ldb ? p.ldb : (bk ? K : N);
+  const long long unit = 16 / (long long)sizeof(T);  // elements per 16 bytes
+  auto aligned = [&](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (!aligned(p.A) || !aligned(p.B) || lda % unit || ldb % unit || p.sA % unit || p.sB % unit) return false;
+  if (!ak && M % unit) return false;  // rows of the A stage are m-contiguous: partial rows copy M - m0 elements
+  if (!bk && N % unit) return false;
+  return true;
 }
 
 }  // namespace
@@ -274,6 +558,17 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
   }
   dim3 grid(tiles_m * tiles_n, chains, splits);
   GemmParams q = p;
+  // grouped raster only where a B tile column is worth keeping in L2 (long K): the K = 32 / 128
+  // trailing updates of the blocked QR stream C and measured faster in row-major order
+  static const int raster_env = [] {
+    const char* e = getenv("TTG_GEMM_RASTER");
+    return e ? atoi(e) : 16;
+  }();
+  static const int raster_kmin = [] {
+    const char* e = getenv("TTG_GEMM_RASTER_KMIN");
+    return e ? atoi(e) : 512;
+  }();
+  q.raster = (kmax >= raster_kmin || (p.K.idx < 0 && p.K.mult >= raster_kmin)) ? raster_env : 0;
   if (splits > 1) {  // partial tiles in a stream-ordered workspace, reduced in fixed order (deterministic)
     q.ws_m = mmax;
     q.ws_n = nmax;
@@ -281,11 +576,12 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
     if (e != cudaSuccess) return e;
   }
   cudaError_t e;
+  const bool tma = gemm_tma_ok<T>(q, opA, opB);
   switch (opA) {
-    case OP_N: e = launch_b<T, OP_N>(q, opB, grid, tiles_n, s); break;
-    case OP_T: e = launch_b<T, OP_T>(q, opB, grid, tiles_n, s); break;
-    case OP_C: e = launch_b<T, OP_C>(q, opB, grid, tiles_n, s); break;
-    default: e = launch_b<T, OP_R>(q, opB, grid, tiles_n, s); break;
+    case OP_N: e = launch_b<T, OP_N>(q, opB, grid, tiles_m, tiles_n, tma, s); break;
+    case OP_T: e = launch_b<T, OP_T>(q, opB, grid, tiles_m, tiles_n, tma, s); break;
+    case OP_C: e = launch_b<T, OP_C>(q, opB, grid, tiles_m, tiles_n, tma, s); break;
+    default: e = launch_b<T, OP_R>(q, opB, grid, tiles_m, tiles_n, tma, s); break;
   }
   if (splits > 1) {
     if (e == cudaSuccess) {

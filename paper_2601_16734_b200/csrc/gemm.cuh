@@ -32,6 +32,7 @@ struct GemmParams {
   // 1: op(A) = A (OP_N / OP_R) is upper triangular or trapezoidal (A[i][k] = 0 for k < i), e.g. the R
   // factor carried into the next site (mps.hpp:202): output row tiles skip the k range left of the diagonal
   int a_upper = 0;
+  int raster = 0;  // set by gemm(): tile rows per raster group (<= 1: row-major)
 };
 
 // Host launcher.  mmax/nmax bound M and N over all chains (grid sizing only);
