@@ -1179,7 +1179,11 @@ ttg_status ttg_create(int device, ttg_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return TTG_CUDA;
   auto* c = new ttg_ctx();
   c->device = device;
-  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+  // highest priority: the context stream carries the latency-critical chain (panels, splits); the
+  // blocked QR's far updates run on a lowest-priority auxiliary stream (qr.cu, lookahead)
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->own, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return TTG_CUDA;
   }

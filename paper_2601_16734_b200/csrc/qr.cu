@@ -1450,6 +1450,48 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
                              (int)t_combine_smem<T>());
     if (e != cudaSuccess) return e;
   }
+  // Panel lookahead (single chain, two-level, tall and wide): see `outer`.  TTG_QR_LOOKAHEAD=0 disables.
+  struct Lookahead {
+    bool on = false, pending = false;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_block = nullptr, ev_far = nullptr;
+    void *W1 = nullptr, *W2 = nullptr;
+  } la;
+  {
+    static const bool la_env = [] {
+      const char* ev = std::getenv("TTG_QR_LOOKAHEAD");
+      return !(ev && ev[0] == '0');
+    }();
+    static cudaStream_t aux_stream = nullptr;  // one process per GPU: one auxiliary stream per process
+    static cudaEvent_t evs[2] = {nullptr, nullptr};
+    if (la_env && two_level && chains == 1 && m >= 2048 && n >= 4 * QR_NBO) {
+      if (!aux_stream) {
+        // lowest priority: the panel stream's cluster kernels are placed before pending update CTAs
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&aux_stream, cudaStreamNonBlocking, lo) != cudaSuccess) aux_stream = nullptr;
+        if (aux_stream && (cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming) != cudaSuccess)) {
+          cudaStreamDestroy(aux_stream);
+          aux_stream = nullptr;
+        }
+        cudaGetLastError();
+      }
+      if (aux_stream) {
+        const size_t wb = (size_t)QR_NBO * n * sizeof(T);
+        if (cudaMallocAsync(&la.W1, wb, s) == cudaSuccess && cudaMallocAsync(&la.W2, wb, s) == cudaSuccess) {
+          la.on = true;
+          la.aux = aux_stream;
+          la.ev_block = evs[0];
+          la.ev_far = evs[1];
+        } else {
+          if (la.W1) cudaFreeAsync(la.W1, s);
+          la.W1 = la.W2 = nullptr;
+          cudaGetLastError();
+        }
+      }
+    }
+  }
   // outer block: S = V_O^H V_O, T_O (t_combine); far columns [jend, n) -= V_O T_O^H V_O^H A
   auto outer = [&](int J0, int jend, bool far) -> cudaError_t {
     const int jbo = jend - J0, mpo = m - J0;
@@ -1464,26 +1506,45 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     t_combine_kernel<T><<<chains, 256, t_combine_smem<T>(), s>>>(
         Sbuf, jbo, Tt + (size_t)(J0 / QR_NB) * QR_NB * QR_NB, To, jbo, w.sT);
     nl += 2;
-    const int nt = n - jend;
-    if (!far || nt <= 0) return cudaGetLastError();
-    GemmParams g1{V + (size_t)J0 * k + J0, A + (size_t)J0 * n + jend, w.W1, w.sV, w.sA, w.sW, dconst(jbo), dconst(nt),
-                  dconst(mpo), nullptr, 0, nullptr, 1.0, 0};
-    g1.lda = k;
-    g1.ldb = n;
-    g1.ldc = nt;
-    if ((e2 = gemm<T>(g1, OP_C, OP_N, jbo, nt, chains, s, mpo)) != cudaSuccess) return e2;
-    GemmParams g2{To, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jbo), dconst(nt), dconst(jbo), nullptr, 0, nullptr, 1.0, 0};
-    g2.lda = QR_NBO;
-    g2.ldb = nt;
-    g2.ldc = nt;
-    if ((e2 = gemm<T>(g2, OP_C, OP_N, jbo, nt, chains, s)) != cudaSuccess) return e2;
-    GemmParams g3{V + (size_t)J0 * k + J0, w.W2, A + (size_t)J0 * n + jend, w.sV, w.sW, w.sA, dconst(mpo), dconst(nt),
-                  dconst(jbo), nullptr, 0, nullptr, -1.0, 1};
-    g3.lda = k;
-    g3.ldb = nt;
-    g3.ldc = n;
-    if ((e2 = gemm<T>(g3, OP_N, OP_N, mpo, nt, chains, s)) != cudaSuccess) return e2;
-    nl += 3;
+    if (!far || n - jend <= 0) return cudaGetLastError();
+    // columns [c0, c1) -= V_O T_O^H V_O^H A on stream `st` with the scratch pair (W1_, W2_)
+    auto far_update = [&](int c0, int c1, void* W1_, void* W2_, cudaStream_t st) -> cudaError_t {
+      const int nt = c1 - c0;
+      cudaError_t e3;
+      GemmParams g1{V + (size_t)J0 * k + J0, A + (size_t)J0 * n + c0, W1_, w.sV, w.sA, w.sW, dconst(jbo), dconst(nt),
+                    dconst(mpo), nullptr, 0, nullptr, 1.0, 0};
+      g1.lda = k;
+      g1.ldb = n;
+      g1.ldc = nt;
+      if ((e3 = gemm<T>(g1, OP_C, OP_N, jbo, nt, chains, st, mpo)) != cudaSuccess) return e3;
+      GemmParams g2{To, W1_, W2_, w.sT, w.sW, w.sW, dconst(jbo), dconst(nt), dconst(jbo), nullptr, 0, nullptr, 1.0, 0};
+      g2.lda = QR_NBO;
+      g2.ldb = nt;
+      g2.ldc = nt;
+      if ((e3 = gemm<T>(g2, OP_C, OP_N, jbo, nt, chains, st)) != cudaSuccess) return e3;
+      GemmParams g3{V + (size_t)J0 * k + J0, W2_, A + (size_t)J0 * n + c0, w.sV, w.sW, w.sA, dconst(mpo), dconst(nt),
+                    dconst(jbo), nullptr, 0, nullptr, -1.0, 1};
+      g3.lda = k;
+      g3.ldb = nt;
+      g3.ldc = n;
+      if ((e3 = gemm<T>(g3, OP_N, OP_N, mpo, nt, chains, st)) != cudaSuccess) return e3;
+      nl += 3;
+      return cudaSuccess;
+    };
+    if (!la.on) return far_update(jend, n, w.W1, w.W2, s);
+    // Lookahead: the next outer block's columns are updated on the panel stream; the rest of the
+    // trailing matrix is updated on the auxiliary stream while the next block's panels are factored.
+    const int jn = jend + QR_NBO < n ? jend + QR_NBO : n;
+    if (la.pending && (e2 = cudaStreamWaitEvent(s, la.ev_far, 0)) != cudaSuccess) return e2;  // previous far update
+    la.pending = false;
+    if ((e2 = far_update(jend, jn, w.W1, w.W2, s)) != cudaSuccess) return e2;
+    if (jn < n) {
+      if ((e2 = cudaEventRecord(la.ev_block, s)) != cudaSuccess) return e2;
+      if ((e2 = cudaStreamWaitEvent(la.aux, la.ev_block, 0)) != cudaSuccess) return e2;
+      if ((e2 = far_update(jn, n, la.W1, la.W2, la.aux)) != cudaSuccess) return e2;
+      if ((e2 = cudaEventRecord(la.ev_far, la.aux)) != cudaSuccess) return e2;
+      la.pending = true;
+    }
     return cudaSuccess;
   };
   const size_t panel_bytes_max = (size_t)m * QR_NB * sizeof(T);
@@ -1606,6 +1667,11 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     }
     if (two_level && j0 + jb == jend && (jend < n || p.Q || w.keep_wy))
       if ((e = outer(J0, jend, jend < n)) != cudaSuccess) return e;
+  }
+  if (la.on) {  // join the auxiliary stream before R / Q are formed and the scratch is released
+    if (la.pending && (e = cudaStreamWaitEvent(s, la.ev_far, 0)) != cudaSuccess) return e;
+    cudaFreeAsync(la.W1, s);
+    cudaFreeAsync(la.W2, s);
   }
   if (coop_part) cudaFreeAsync(coop_part, s);
   upper_kernel<T><<<dim3(blocks_for((long long)k * n), chains), 256, 0, s>>>(A, w.sA, n, static_cast<T*>(p.R), p.sR, k);
