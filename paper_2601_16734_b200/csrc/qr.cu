@@ -1464,7 +1464,13 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     }();
     static cudaStream_t aux_stream = nullptr;  // one process per GPU: one auxiliary stream per process
     static cudaEvent_t evs[2] = {nullptr, nullptr};
-    if (la_env && two_level && chains == 1 && m >= 2048 && n >= 4 * QR_NBO) {
+    static const int la1_rows = [] {  // rank-32 (single-level) lookahead from this many rows on; 0 = off
+      const char* ev = std::getenv("TTG_QR_LOOKAHEAD1");
+      return ev ? std::atoi(ev) : 0;  // measured: C4 2078 -> 2087 ms with 512 (tiny updates, event traffic)
+    }();
+    const bool la2 = two_level && m >= 2048 && n >= 4 * QR_NBO;
+    const bool la1 = !two_level && la1_rows > 0 && m >= la1_rows && n >= 8 * QR_NB;
+    if (la_env && chains == 1 && (la2 || la1)) {
       if (!aux_stream) {
         // lowest priority: the panel stream's cluster kernels are placed before pending update CTAs
         int lo = 0, hi = 0;
@@ -1642,28 +1648,51 @@ cudaError_t householder_qr_blocked(const QrParams& p, const QrBlockedWork& w, in
     const int jend = two_level ? (J0 + QR_NBO < k ? J0 + QR_NBO : k) : n;  // inner updates stop at the block end
     const int nt = jend - j0 - jb;
     if (nt > 0) {
-      // W1 = V^H A_trail (jb x nt)
-      GemmParams g1{V + (size_t)j0 * k + j0, A + (size_t)j0 * n + j0 + jb, w.W1, w.sV, w.sA, w.sW, dconst(jb), dconst(nt),
-                    dconst(mp), nullptr, 0, nullptr, 1.0, 0};
-      g1.lda = k;
-      g1.ldb = n;
-      g1.ldc = nt;
-      if ((e = gemm<T>(g1, OP_C, OP_N, jb, nt, chains, s, mp)) != cudaSuccess) return e;
-      // W2 = T^H W1
-      GemmParams g2{Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, w.W1, w.W2, w.sT, w.sW, w.sW, dconst(jb), dconst(nt),
-                    dconst(jb), nullptr, 0, nullptr, 1.0, 0};
-      g2.lda = QR_NB;
-      g2.ldb = nt;
-      g2.ldc = nt;
-      if ((e = gemm<T>(g2, OP_C, OP_N, jb, nt, chains, s)) != cudaSuccess) return e;
-      // A_trail -= V W2
-      GemmParams g3{V + (size_t)j0 * k + j0, w.W2, A + (size_t)j0 * n + j0 + jb, w.sV, w.sW, w.sA, dconst(mp), dconst(nt),
-                    dconst(jb), nullptr, 0, nullptr, -1.0, 1};
-      g3.lda = k;
-      g3.ldb = nt;
-      g3.ldc = n;
-      if ((e = gemm<T>(g3, OP_N, OP_N, mp, nt, chains, s)) != cudaSuccess) return e;
-      nl += 3;
+      // columns [c0, c1) -= V T^H V^H A for this panel's reflectors
+      auto panel_update = [&](int c0, int c1, void* W1_, void* W2_, cudaStream_t st) -> cudaError_t {
+        const int ntc = c1 - c0;
+        cudaError_t e3;
+        // W1 = V^H A_trail (jb x ntc)
+        GemmParams g1{V + (size_t)j0 * k + j0, A + (size_t)j0 * n + c0, W1_, w.sV, w.sA, w.sW, dconst(jb), dconst(ntc),
+                      dconst(mp), nullptr, 0, nullptr, 1.0, 0};
+        g1.lda = k;
+        g1.ldb = n;
+        g1.ldc = ntc;
+        if ((e3 = gemm<T>(g1, OP_C, OP_N, jb, ntc, chains, st, mp)) != cudaSuccess) return e3;
+        // W2 = T^H W1
+        GemmParams g2{Tt + (size_t)(j0 / QR_NB) * QR_NB * QR_NB, W1_, W2_, w.sT, w.sW, w.sW, dconst(jb), dconst(ntc),
+                      dconst(jb), nullptr, 0, nullptr, 1.0, 0};
+        g2.lda = QR_NB;
+        g2.ldb = ntc;
+        g2.ldc = ntc;
+        if ((e3 = gemm<T>(g2, OP_C, OP_N, jb, ntc, chains, st)) != cudaSuccess) return e3;
+        // A_trail -= V W2
+        GemmParams g3{V + (size_t)j0 * k + j0, W2_, A + (size_t)j0 * n + c0, w.sV, w.sW, w.sA, dconst(mp), dconst(ntc),
+                      dconst(jb), nullptr, 0, nullptr, -1.0, 1};
+        g3.lda = k;
+        g3.ldb = ntc;
+        g3.ldc = n;
+        if ((e3 = gemm<T>(g3, OP_N, OP_N, mp, ntc, chains, st)) != cudaSuccess) return e3;
+        nl += 3;
+        return cudaSuccess;
+      };
+      const int c_lo = j0 + jb;
+      if (la.on && !two_level) {
+        // rank-32 lookahead: the next panel's columns on the panel stream, the rest behind it
+        const int jn = c_lo + QR_NB < jend ? c_lo + QR_NB : jend;
+        if (la.pending && (e = cudaStreamWaitEvent(s, la.ev_far, 0)) != cudaSuccess) return e;
+        la.pending = false;
+        if ((e = panel_update(c_lo, jn, w.W1, w.W2, s)) != cudaSuccess) return e;
+        if (jn < jend) {
+          if ((e = cudaEventRecord(la.ev_block, s)) != cudaSuccess) return e;
+          if ((e = cudaStreamWaitEvent(la.aux, la.ev_block, 0)) != cudaSuccess) return e;
+          if ((e = panel_update(jn, jend, la.W1, la.W2, la.aux)) != cudaSuccess) return e;
+          if ((e = cudaEventRecord(la.ev_far, la.aux)) != cudaSuccess) return e;
+          la.pending = true;
+        }
+      } else if ((e = panel_update(c_lo, jend, w.W1, w.W2, s)) != cudaSuccess) {
+        return e;
+      }
     }
     if (two_level && j0 + jb == jend && (jend < n || p.Q || w.keep_wy))
       if ((e = outer(J0, jend, jend < n)) != cudaSuccess) return e;
