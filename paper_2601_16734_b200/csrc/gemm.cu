@@ -552,8 +552,16 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
   // blocked QR: 32 x n x m)
   int splits = 1;
   const long long tiles = (long long)tiles_m * tiles_n * chains;
-  if (kmax >= 1024 && tiles < 2 * 148) {
-    splits = (int)std::min<long long>((2 * 148 + tiles - 1) / tiles, kmax / 256);
+  static const int splitk_min = [] {  // split-K from this K on (TTG_GEMM_SPLITK_MIN)
+    const char* e = getenv("TTG_GEMM_SPLITK_MIN");
+    return e ? atoi(e) : 256;
+  }();
+  if (kmax >= splitk_min && tiles < 2 * 148) {
+    static const int splitk_div = [] {  // at least this much K per split (TTG_GEMM_SPLITK_DIV)
+      const char* e = getenv("TTG_GEMM_SPLITK_DIV");
+      return e ? atoi(e) : 64;  // C4 A/B (K >= / K per split): 1024/256 1913 ms, 512/128 1833 ms, 256/64 1816 ms, 128/32 1814 ms
+    }();
+    splits = (int)std::min<long long>((2 * 148 + tiles - 1) / tiles, kmax / splitk_div);
     splits = std::max(1, std::min(splits, 64));
   }
   dim3 grid(tiles_m * tiles_n, chains, splits);
