@@ -438,6 +438,30 @@ void Engine<T>::split_preconditioned(const void* theta, long long s_theta, DimEx
         const double b = std::min(Lr.eval(hb.data(), c, ld), Kc.eval(hb.data(), c, ld));
         qflops += (Scalar<T>::is_complex ? 4.0 : 1.0) * 6.0 * b * b * (a - b / 3.0);
       }
+  // TTG_PRE_SMALL=1: one R-only QR as for the large splits (split_large): mode 0 factors theta^H = Q R
+  // and rotates the columns of L = R^H (same left singular vectors as theta), mode 1 factors theta = Q R
+  // and rotates R in mode 1 (same right singular vectors); the isometry comes straight out of the Jacobi
+  // epilogue, no Q, no second QR, no isometry GEMM.
+  // Measured: single chains (C2) 125.1 -> 116.3 ms per call; batches (C5) 1347 -> 1447 ms (21% more
+  // Jacobi sweeps, and the batched splits are Jacobi-bound), so batches keep the two-QR form.
+  static const int pre_small = [] {
+    const char* e = getenv("TTG_PRE_SMALL");
+    return e ? atoi(e) : 0;
+  }();
+  if (pre_small == 1 || (pre_small == 0 && B == 1)) {
+    {
+      ProfScope ps(ctx, TTG_PROF_QR, qflops / 3.0);
+      // mode 0: M_ = theta^H (n x m), output R^H = L (m x r0); mode 1: M_ = theta (m x n), output R (r0 x n)
+      CK(qr_precondition<T>(theta, s_theta, M, N, mode == 0 ? 1 : 2, d_bonds, ld, pre_slot, nullptr, 0, Lb, sp,
+                            mode == 0 ? ub(N) : ub(M), mode == 0 ? ub(M) : ub(N), stp, B, st));
+    }
+    ++ctx->launches;
+    if (mode == 0)
+      S(Lb, sp, M, R0, out_idx, iso, s_iso, 0, tol, max_bond, check_active, accumulate, work, s_work, Warm(), true);
+    else
+      S(Lb, sp, R0, N, out_idx, iso, s_iso, 1, tol, max_bond, check_active, accumulate, work, s_work, Warm(), true);
+    return;
+  }
   {
     ProfScope ps(ctx, TTG_PROF_QR, qflops);
     CK(qr_precondition<T>(theta, s_theta, M, N, mode, d_bonds, ld, pre_slot, Qb, sp, R1h, sp, lu, ku, stp, B, st));

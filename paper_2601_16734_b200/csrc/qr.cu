@@ -308,6 +308,8 @@ __global__ void __launch_bounds__(QR_THREADS) qr_pre_kernel(const T* A, long lon
   const int chain = blockIdx.x;
   if (st && !st[chain].active) return;
   const int mi = Md.eval(bonds, chain, ld), ni = Nd.eval(bonds, chain, ld);
+  const bool out_r = (trans & 2) != 0;  // write R (r0 x k) instead of R^H
+  trans &= 1;
   const int l = trans ? ni : mi, k = trans ? mi : ni, r0 = min(l, k);
   const int lw = l | 1;  // odd column stride: transposing loads/stores are bank-conflict free
   A += sA * chain;
@@ -371,11 +373,18 @@ __global__ void __launch_bounds__(QR_THREADS) qr_pre_kernel(const T* A, long lon
     apply_reflector_cols<T>(Wk, l, lw, v, j, conj_(s_tau), j + 1, k, warp, nwarps, lane);
     __syncthreads();
   }
-  // R1^H (k x r0): RH[c, i] = conj(R1[i, c]) for c >= i
+  // R1^H (k x r0): RH[c, i] = conj(R1[i, c]) for c >= i; with trans & 2: R1 itself (r0 x k)
   T* rh = RH + sRH * chain;
-  for (int idx = tid; idx < k * r0; idx += blockDim.x) {
-    const int c = idx / r0, i = idx % r0;
-    rh[idx] = (c >= i) ? conj_(Wk[c * lw + i]) : Scalar<T>::zero();
+  if (out_r) {
+    for (int idx = tid; idx < r0 * k; idx += blockDim.x) {
+      const int i = idx / k, c = idx % k;
+      rh[idx] = (c >= i) ? Wk[c * lw + i] : Scalar<T>::zero();
+    }
+  } else {
+    for (int idx = tid; idx < k * r0; idx += blockDim.x) {
+      const int c = idx / r0, i = idx % r0;
+      rh[idx] = (c >= i) ? conj_(Wk[c * lw + i]) : Scalar<T>::zero();
+    }
   }
   if (tid == 0) bonds[chain * ld + out_idx] = r0;
   if (!Q) return;

@@ -343,6 +343,8 @@ __global__ void __launch_bounds__(QRS_THREADS, 1)
   const int chain = blockIdx.x;
   if (st && !st[chain].active) return;
   const int mi = Md.eval(bonds, chain, ld), ni = Nd.eval(bonds, chain, ld);
+  const bool out_r = (trans & 2) != 0;  // write R (r0 x k) instead of R^H
+  trans &= 1;
   const int l = trans ? ni : mi, k = trans ? mi : ni, r0 = min(l, k);
   const SmallLayout Ly = small_layout(l, k, NB);
   const int lw = Ly.lw;
@@ -523,11 +525,18 @@ __global__ void __launch_bounds__(QRS_THREADS, 1)
     minus_v_times<T, NB>(Wk, k, lw, l, j0, nb, j0 + nb, nt, W2, ldw, 0);
     __syncthreads();
   }
-  // R1^H (k x r0): RH[c, i] = conj(R1[i, c]) for c >= i
+  // R1^H (k x r0): RH[c, i] = conj(R1[i, c]) for c >= i; with trans & 2: R1 itself (r0 x k)
   T* rh = RH + sRH * chain;
-  for (int idx = tid; idx < k * r0; idx += QRS_THREADS) {
-    const int c = idx / r0, i = idx % r0;
-    rh[idx] = (c >= i) ? conj_(Wk[(long long)c * lw + i]) : Scalar<T>::zero();
+  if (out_r) {
+    for (int idx = tid; idx < r0 * k; idx += QRS_THREADS) {
+      const int i = idx / k, c = idx % k;
+      rh[idx] = (c >= i) ? Wk[(long long)c * lw + i] : Scalar<T>::zero();
+    }
+  } else {
+    for (int idx = tid; idx < k * r0; idx += QRS_THREADS) {
+      const int c = idx / r0, i = idx % r0;
+      rh[idx] = (c >= i) ? conj_(Wk[(long long)c * lw + i]) : Scalar<T>::zero();
+    }
   }
   if (tid == 0) bonds[chain * ld + out_idx] = r0;
   if (!Q) return;
