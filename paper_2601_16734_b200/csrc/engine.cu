@@ -289,7 +289,7 @@ struct Engine {
     SvdParams p{};
     static const int no_early = [] {
       const char* e = getenv("TTG_SVD_EARLY");
-      return (e && e[0] == '0') ? 1 : 0;
+      return (e && e[0] == '0') ? 1 : (e && e[0] == '2') ? 2 : 0;
     }();
     p.no_early = no_early;
     p.theta_pre = w.pre;

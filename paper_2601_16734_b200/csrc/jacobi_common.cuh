@@ -45,7 +45,8 @@ __device__ __forceinline__ void finish_status(const SvdParams& p, ChainState* st
 // (C2: 7.8 -> 6.9 sweeps per split, same singular values and isometries).
 // TTG_SVD_EARLY=0 (p.no_early) restores the check sweep.
 __device__ __forceinline__ double early_stop2(const SvdParams& p, double tol_rot) {
-  return p.no_early ? tol_rot * tol_rot : fmax(tol_rot * tol_rot, 0.01 * tol_rot);
+  // no_early: 0 = default margin (cos^2 <= tol_rot / 100), 1 = no early stop, 2 = cos^2 <= tol_rot / 10 (experiment)
+  return p.no_early == 1 ? tol_rot * tol_rot : fmax(tol_rot * tol_rot, (p.no_early == 2 ? 0.1 : 0.01) * tol_rot);
 }
 
 // 1/sqrt(w) for w in [1, 2]: single-precision seed + two Newton steps (full double)
@@ -150,13 +151,17 @@ struct GridMeta {
 // Stop rule of the grid kernels.  A sweep whose rotations all had cos^2 <= tol^2
 // rotated nothing: converged.  The early stop (largest rotated cos^2 <= big2, see
 // early_stop2) assumes quadratic convergence; it is taken only when the sweep's
-// largest cos^2 is also <= 100 x (previous sweep's)^2, i.e. when the decay was
-// quadratic.  Clustered singular values converge linearly and keep sweeping
-// until a sweep rotates nothing above the threshold.
+// largest cos^2 is also <= 1e4 x (previous sweep's)^2, i.e. when the decay was
+// quadratic: cos_next <= 100 cos^2.  Measured on the C4 splits (1024 columns,
+// TTG_BG_DEBUG): cos^2 per sweep ... 8.9e-6, 7.0e-10, 9.5e-17, 0, i.e. cos_next =
+// 3 .. 20 cos^2, and a factor of 100 on cos^2 (10 on the cosine) sent most splits
+// into an all-skipped check sweep.  Clustered singular values converge linearly
+// (cos^2_next ~ rho cos^2, ratio to the square >> 1e4 at this level) and keep
+// sweeping until a sweep rotates nothing above the threshold.
 __device__ __forceinline__ bool grid_converged(const GridMeta* mt, int sweep, double tol2, double big2) {
   const double c2 = (double)__uint_as_float(mt->c2bits[sweep % 3]);
   const double prev = sweep > 0 ? (double)__uint_as_float(mt->c2bits[(sweep + 2) % 3]) : 1.0;
-  return c2 <= tol2 || (c2 <= big2 && c2 <= 100.0 * prev * prev);
+  return c2 <= tol2 || (c2 <= big2 && c2 <= 1.0e4 * prev * prev);
 }
 
 // Epilogue of the grid Jacobi kernels: exact column norms, descending order, truncation
