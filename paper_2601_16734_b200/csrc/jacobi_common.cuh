@@ -44,6 +44,12 @@ __device__ __forceinline__ void finish_status(const SvdParams& p, ChainState* st
 // iteration, which drops the final all-skipped check sweep in most splits
 // (C2: 7.8 -> 6.9 sweeps per split, same singular values and isometries).
 // TTG_SVD_EARLY=0 (p.no_early) restores the check sweep.
+// Ring kernels (one CTA or one cluster per chain, unpreconditioned or small splits): clustered
+// singular values (sigma = 1 +- 1e-9 blocks, tools/orth_probe.py) left cosines of 6000 cos^2 behind a
+// sweep that looked quadratic, so their early stop keeps a factor 1e4 instead of 100.
+__device__ __forceinline__ double early_stop2_ring(const SvdParams& p, double tol_rot) {
+  return p.no_early == 1 ? tol_rot * tol_rot : fmax(tol_rot * tol_rot, 1.0e-4 * tol_rot);
+}
 __device__ __forceinline__ double early_stop2(const SvdParams& p, double tol_rot) {
   // no_early: 0 = default margin (cos^2 <= tol_rot / 100), 1 = no early stop, 2 = cos^2 <= tol_rot / 10 (experiment)
   return p.no_early == 1 ? tol_rot * tol_rot : fmax(tol_rot * tol_rot, (p.no_early == 2 ? 0.1 : 0.01) * tol_rot);
@@ -89,6 +95,45 @@ __device__ __forceinline__ double ring_tan(double alpha, double beta, double g) 
   r = r * fma(-num, r, 2.0);
   const double tt = 0.5 * den * r;
   return den < 1e-30 ? tt : (double)tf;
+}
+
+__device__ __forceinline__ float bg_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float bg_rsqrt(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Rotation of a pair from (alpha, beta, g = |inner product| > 0): tangent t (signed like beta - alpha)
+// and cosine c = (1 + t^2)^-1/2 with c accurate to double precision (the rotation must be orthogonal
+// to rounding; the angle itself only needs single precision).  alpha, beta, g are scaled into float
+// range by an exact power of two (g <= sqrt(alpha beta) <= max(alpha, beta), so the larger high word
+// gives the exponent).  With fn = (beta - alpha) f, fd = 2 g f and r = sqrt(fn^2 + fd^2):
+//   t = fd / (|fn| + r)           (= 1 / (|zeta| + sqrt(1 + zeta^2)), zeta = fn / fd; no case split,
+//                                  and the tiny-angle limit g / (beta - alpha) comes out by itself)
+//   c^2 = (|fn| + r) / (2 r)      (half-angle), so the seed of c needs no extra dependent MUFU:
+//                                  rcp(|fn| + r) and rsqrt(c^2) issue together
+// followed by one Halley step for c in double (seed error 2^-22 -> ~1e-20).
+__device__ __forceinline__ void bg_rotation(double alpha, double beta, double g, double& t, double& c) {
+  int eb = (max(__double2hiint(alpha), __double2hiint(beta)) >> 20) & 0x7ff;
+  eb = eb > 2045 ? 2045 : eb;
+  const double f = __hiloint2double((2046 - eb) << 20, 0);
+  const float fn = (float)((beta - alpha) * f), fd = (float)(2.0 * g * f);  // |fn| < 2, 0 <= fd < 4
+  const float an = fabsf(fn);
+  const float s2 = fmaf(fn, fn, fd * fd);
+  const float rs = bg_rsqrt(s2);           // 1 / r
+  const float den = fmaf(s2, rs, an);      // |fn| + r
+  const float tf = fd * bg_rcp(den);
+  const float c2 = 0.5f * den * rs;        // cos^2 in [1/2, 1]
+  const float cf = c2 * bg_rsqrt(c2);
+  t = (double)copysignf(tf, fn);
+  const double w = fma(t, t, 1.0), y = (double)cf;
+  const double e = fma(-w, y * y, 1.0);
+  c = fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 namespace cg = cooperative_groups;
@@ -146,6 +191,7 @@ struct GridMeta {
   double f2;
   int bad, rank, flag[2], sweeps, full;
   unsigned c2bits[3];  // largest rotated cos^2 of sweep s in slot s % 3 (float bits, atomicMax)
+  unsigned tc2bits[3]; // largest (t cos)^2 of the sweep's rotations, same slots (kernels that track it)
 };
 
 // Stop rule of the grid kernels.  A sweep whose rotations all had cos^2 <= tol^2
@@ -158,10 +204,17 @@ struct GridMeta {
 // into an all-skipped check sweep.  Clustered singular values converge linearly
 // (cos^2_next ~ rho cos^2, ratio to the square >> 1e4 at this level) and keep
 // sweeping until a sweep rotates nothing above the threshold.
-__device__ __forceinline__ bool grid_converged(const GridMeta* mt, int sweep, double tol2, double big2) {
+__device__ __forceinline__ bool grid_converged(const GridMeta* mt, int sweep, double tol2, double big2,
+                                               double tol_rot = 0.0, bool guarded = false) {
   const double c2 = (double)__uint_as_float(mt->c2bits[sweep % 3]);
   const double prev = sweep > 0 ? (double)__uint_as_float(mt->c2bits[(sweep + 2) % 3]) : 1.0;
-  return c2 <= tol2 || (c2 <= big2 && c2 <= 1.0e4 * prev * prev);
+  // Early stop only for kernels that track (t cos)^2 (guarded): small rotation angles are what
+  // near-degenerate singular values violate (see sweep_stop in jacobi_svd.cu); the others always end
+  // with a sweep that rotates nothing.
+  if (c2 <= tol2) return true;
+  if (!guarded) return false;
+  const double tc2 = (double)__uint_as_float(mt->tc2bits[sweep % 3]);
+  return c2 <= big2 && c2 <= 1.0e4 * prev * prev && tc2 <= 0.01 * tol_rot * tol_rot;
 }
 
 // Epilogue of the grid Jacobi kernels: exact column norms, descending order, truncation
