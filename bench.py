@@ -274,8 +274,8 @@ def _workload_desc(cfg):
 # traffic is about one read of the matrix per launch
 _SVD_TRAFFIC = {"C2": {"kernel": "jacobi_cluster_kernel<double,16,8,128,2>", "bytes": 204117},
                 # round 2: block-Gram Jacobi on a 1024 x 1024 split (profiles/r02_jbg_c4.raw.csv: 8.46 MB read +
-                # 2.26 MB written for the 8 MiB matrix, 16.98 ms)
-                "C4": {"kernel": "jacobi_bg_kernel<16,256>", "bytes": 10720256}}
+                # 1.92 MB written for the 8 MiB matrix, 14.0 ms)
+                "C4": {"kernel": "jacobi_bg_kernel<16,256>", "bytes": 10379520}}
 
 
 def _roofline(prof, cfg_name=None):
