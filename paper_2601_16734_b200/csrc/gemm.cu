@@ -468,24 +468,32 @@ __global__ void __launch_bounds__(NTHREADS) gemm_kernel(GemmParams p, int tiles_
       }
 }
 
-// Deterministic split-K: C (+)= sum over splits in split order.
+// Deterministic split-K: C (+)= sum over splits in split order.  One thread per output element
+// (blockIdx.y = row, no index division), the partials of eight splits in flight before they are added
+// in order.
 template <typename T>
-__global__ void splitk_reduce_kernel(GemmParams p, int splits) {
-  const int chain = blockIdx.y;
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmParams p, int splits) {
+  const int chain = blockIdx.z;
   if (p.st && !p.st[chain].active) return;
   const int M = p.M.eval(p.bonds, chain, p.bonds_ld);
   const int N = p.N.eval(p.bonds, chain, p.bonds_ld);
+  const int m = blockIdx.y, n = blockIdx.x * 256 + threadIdx.x;
+  if (m >= M || n >= N) return;
   const long long ldc = p.ldc ? p.ldc : N;
-  T* C = static_cast<T*>(p.C) + p.sC * chain;
-  const T* w = static_cast<const T*>(p.ws) + (long long)chain * splits * p.ws_m * p.ws_n;
+  T* dst = static_cast<T*>(p.C) + p.sC * chain + m * ldc + n;
   const long long plane = (long long)p.ws_m * p.ws_n;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)M * N;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long m = idx / N, n = idx % N;
-    T acc = p.beta ? C[m * ldc + n] : Scalar<T>::zero();
-    for (int z = 0; z < splits; ++z) acc = add(acc, w[z * plane + m * p.ws_n + n]);
-    C[m * ldc + n] = acc;
+  const T* w = static_cast<const T*>(p.ws) + (long long)chain * splits * plane + (long long)m * p.ws_n + n;
+  T acc = p.beta ? *dst : Scalar<T>::zero();
+  int z = 0;
+  for (; z + 8 <= splits; z += 8) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = w[(z + u) * plane];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = add(acc, v[u]);
   }
+  for (; z < splits; ++z) acc = add(acc, w[z * plane]);
+  *dst = acc;
 }
 
 template <typename T, int OPA, int OPB>
@@ -593,8 +601,7 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
   }
   if (splits > 1) {
     if (e == cudaSuccess) {
-      splitk_reduce_kernel<T><<<dim3(std::max(1, std::min(148 * 4, (int)((long long)mmax * nmax / 256 + 1))), chains),
-                                256, 0, s>>>(q, splits);
+      splitk_reduce_kernel<T><<<dim3((nmax + 255) / 256, mmax, chains), 256, 0, s>>>(q, splits);
       e = cudaGetLastError();
     }
     cudaFreeAsync(q.ws, s);
