@@ -1,6 +1,7 @@
 """Kernel-level parity: DMMA GEMM, Householder QR and the truncated Jacobi SVD
 against numpy, through the C-ABI test hooks of libttgpu.so."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -50,6 +51,46 @@ def test_gemm_ops(dtype, opA, opB):
             ref = OPS[opA](A[b]) @ OPS[opB](B[b])
             err = np.abs(got[b] - ref).max() / max(1.0, np.abs(ref).max())
             assert err < 1e-13, (M, N, K, err)
+
+
+_TMA_SNIPPET = """
+import sys
+import numpy as np
+sys.path.insert(0, '.')
+from tests.test_gpu_kernels import OPS, _gemm
+worst = 0.0
+for dtype in (np.float64, np.complex128):
+    for opA in range(4):
+        for opB in range(4):
+            rng = np.random.default_rng(16 * opA + opB)
+            for (M, N, K) in [(128, 96, 192), (64, 190, 64), (200, 130, 256), (70, 66, 1024)]:
+                batch = 2
+                def rnd(*s):
+                    x = rng.standard_normal(s)
+                    return x + 1j * rng.standard_normal(s) if dtype == np.complex128 else x
+                Ash = (batch, M, K) if opA in (0, 3) else (batch, K, M)
+                Bsh = (batch, K, N) if opB in (0, 3) else (batch, N, K)
+                A, B = np.ascontiguousarray(rnd(*Ash)), np.ascontiguousarray(rnd(*Bsh))
+                got = _gemm(opA, opB, A, B, M, N, K, batch)
+                for b in range(batch):
+                    ref = OPS[opA](A[b]) @ OPS[opB](B[b])
+                    worst = max(worst, np.abs(got[b] - ref).max() / max(1.0, np.abs(ref).max()))
+assert worst < 1e-13, worst
+print('TMA_GEMM_OK', worst)
+"""
+
+
+def test_gemm_tma_all_ops():
+    """The TMA-staged GEMM variant (bulk row copies + mbarrier pipeline) for every operand mode and both
+    dtypes (TTG_GEMM_TMA=2 routes all eligible products to it; by default only m-/n-contiguous operand
+    pairs use it), including split-K (K = 1024 with few tiles) and partial edge tiles."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TTG_GEMM_TMA="2")
+    r = subprocess.run([sys.executable, "-c", _TMA_SNIPPET], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "TMA_GEMM_OK" in r.stdout, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("blocked", [False, True])
