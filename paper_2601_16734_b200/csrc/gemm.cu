@@ -5,6 +5,8 @@
 // (complex) fragment loads are bank-conflict free.
 #include "gemm.cuh"
 
+#include <cuda.h>  // CUtensorMap and its enums (types only; the encoder is fetched through the runtime)
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -496,6 +498,189 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmParams p, int sp
   *dst = acc;
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-map TMA variant (f64, one chain, A = OP_N): the stage's A tile (64 rows x 16 k) and B tile arrive
+// by cp.async.bulk.tensor.2d (SASS UTMALDG) into unpadded 128-byte rows with the 128-byte swizzle
+// (16-byte chunk index XOR (row & 7)); out-of-range rows / columns / k are zero-filled by the TMA unit, so
+// ragged edges need no special case.  Fragment loads stay bank-conflict free without padding:
+//   * lane t4 takes the k PAIR (2 t4, 2 t4 + 1) of an 8-k group: one MMA consumes the even, the next the odd
+//     k of the pairs (A and B use the same assignment, the sum over k does not care);
+//   * k-contiguous tiles (A; B for OP_T): one 128-bit load per fragment row gives the pair; fragment row g
+//     maps to tile row phys(g) = ((g & 1) << 2) | (g >> 1), so the two rows of a quarter warp differ in
+//     bit 2 and the XOR spreads the eight lanes over the eight chunks;
+//   * n-contiguous B (OP_N): four boxes of 16 columns per stage; the two k rows of a pair are 64-bit loads
+//     from rows k & 7 in {0, 2, 4, 6} (even MMA) or {1, 3, 5, 7} (odd MMA), which the XOR spreads as well.
+// The output rows (and, for OP_T, columns) are un-permuted in the epilogue.
+// ---------------------------------------------------------------------------
+constexpr int TM_STAGES = 4;
+constexpr int TM_TILE_BYTES = 64 * 128;  // 64 rows (or 4 boxes x 16 rows) of 128 bytes
+constexpr size_t TM_SMEM = (size_t)TM_STAGES * 2 * TM_TILE_BYTES + 1024;  // + alignment slack
+
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ int tm_phys(int g) { return ((g & 1) << 2) | (g >> 1); }
+
+template <int OPB>  // OP_N: B is K x N (n contiguous); OP_T: B is N x K (k contiguous)
+__global__ void __launch_bounds__(NTHREADS) gemm_tm_kernel(GemmParams p, const __grid_constant__ CUtensorMap mapA,
+                                                           const __grid_constant__ CUtensorMap mapB, int tiles_m,
+                                                           int tiles_n) {
+  constexpr int BK = 16;
+  extern __shared__ unsigned char tm_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* As = base;                                  // [stage][64 rows][128 B]
+  unsigned char* Bs = base + TM_STAGES * TM_TILE_BYTES;      // OP_N: [stage][4 boxes][16 k][128 B]; OP_T: as A
+  __shared__ __align__(8) unsigned long long full[TM_STAGES];
+  const int M = p.M.mult, N = p.N.mult, K = p.K.mult;  // host-shaped products only
+  int tm, tn;
+  tile_of(blockIdx.x, tiles_m, tiles_n, p.raster, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= M || n0 >= N) return;
+  const long long ldc = p.ldc ? p.ldc : N;
+  double* C = static_cast<double*>(p.C);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int pg = tm_phys(g);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int st = 0; st < TM_STAGES; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+  auto issue = [&](int stage, int k0) {  // one elected thread
+    mbar_expect_tx(&full[stage], 2 * TM_TILE_BYTES);
+    tma_load_2d(As + stage * TM_TILE_BYTES, &mapA, k0, m0, &full[stage]);
+    if constexpr (OPB == OP_N) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        tma_load_2d(Bs + stage * TM_TILE_BYTES + b * 2048, &mapB, n0 + 16 * b, k0, &full[stage]);
+    } else {
+      tma_load_2d(Bs + stage * TM_TILE_BYTES, &mapB, k0, n0, &full[stage]);
+    }
+  };
+
+  const int ktiles_all = (K + BK - 1) / BK;
+  const int splits = gridDim.z;
+  const int per = (ktiles_all + splits - 1) / splits;
+  int kt0 = blockIdx.z * per;
+  const int kt1 = min(ktiles_all, kt0 + per);
+  if (p.a_upper) kt0 = max(kt0, m0 / BK);
+  const int ktiles = max(0, kt1 - kt0);
+  if (tid == 0)
+    for (int st = 0; st < TM_STAGES - 1 && st < ktiles; ++st) issue(st, (kt0 + st) * BK);
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int stage = kt % TM_STAGES;
+    if (tid == 0 && kt + TM_STAGES - 1 < ktiles) issue((kt + TM_STAGES - 1) % TM_STAGES, (kt0 + kt + TM_STAGES - 1) * BK);
+    mbar_wait(&full[stage], (kt / TM_STAGES) & 1);
+    const unsigned char* at = As + stage * TM_TILE_BYTES;
+    const unsigned char* bt = Bs + stage * TM_TILE_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 8) {
+      const int ch = (kk >> 1) + t4;  // 16-byte chunk of this lane's k pair
+      double2 a[2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = wm + i * 16 + h * 8 + pg;
+          a[i][h] = *reinterpret_cast<const double2*>(at + row * 128 + ((ch ^ (row & 7)) << 4));
+        }
+      double2 b[4];
+      if constexpr (OPB == OP_N) {
+        const int ke = kk + 2 * t4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int n = wn + j * 8 + g;
+          const unsigned char* bx = bt + (n >> 4) * 2048 + (n & 1) * 8;
+          const int c2 = (n & 15) >> 1;
+          b[j].x = *reinterpret_cast<const double*>(bx + ke * 128 + ((c2 ^ (ke & 7)) << 4));
+          b[j].y = *reinterpret_cast<const double*>(bx + (ke + 1) * 128 + ((c2 ^ ((ke + 1) & 7)) << 4));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int row = wn + j * 8 + pg;
+          b[j] = *reinterpret_cast<const double2*>(bt + row * 128 + ((ch ^ (row & 7)) << 4));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma(acc[i][j], a[i][0].x, a[i][1].x, b[j].x);
+          dmma(acc[i][j], a[i][0].y, a[i][1].y, b[j].y);
+        }
+    }
+    __syncthreads();
+  }
+
+  const double alpha = p.alpha;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + wm + i * 16 + (r >= 2 ? 8 : 0) + pg;
+        const int fc = 2 * t4 + (r & 1);  // fragment column
+        const int n = n0 + wn + j * 8 + (OPB == OP_N ? fc : tm_phys(fc));
+        if (m < M && n < N) {
+          double* dst = C + m * ldc + n;
+          if (splits > 1) {
+            double* w = static_cast<double*>(p.ws) + ((long long)blockIdx.z * p.ws_m + m) * p.ws_n + n;
+            *w = alpha * acc[i][j][r];
+          } else {
+            const double v = alpha * acc[i][j][r];
+            *dst = p.beta ? *dst + v : v;
+          }
+        }
+      }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                   const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline EncodeTiledFn tm_encoder() {
+  static const EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+// f64 matrix with `inner` contiguous elements per row, `rows` rows, leading dimension ld: boxes of 16 x box_rows
+inline bool tm_encode(CUtensorMap* map, const void* base, long long inner, long long rows, long long ld, int box_rows) {
+  const EncodeTiledFn enc = tm_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1u, 1u};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, int OPA, int OPB>
 cudaError_t launch_one(const GemmParams& p, dim3 grid, int tiles_m, int tiles_n, bool tma, cudaStream_t s) {
   if (tma) {
@@ -592,6 +777,48 @@ cudaError_t gemm(const GemmParams& p, int opA, int opB, int mmax, int nmax, int 
     if (e != cudaSuccess) return e;
   }
   cudaError_t e;
+  // tensor-map TMA kernel: f64, one chain, host shapes, A = OP_N and B = OP_N / OP_T (the projection chain
+  // X = L T, Y = X T, theta = Y R^T and the carry R T), 16-byte aligned bases and leading dimensions
+  if constexpr (!Scalar<T>::is_complex) {
+    static const int tm_mode = [] {
+      const char* ev = getenv("TTG_GEMM_TM");
+      return ev ? atoi(ev) : 1;
+    }();
+    const bool shapes = q.M.idx < 0 && q.N.idx < 0 && q.K.idx < 0;
+    if (tm_mode && shapes && chains == 1 && q.st == nullptr && opA == OP_N && (opB == OP_N || opB == OP_T)) {
+      const long long M = q.M.mult, N = q.N.mult, K = q.K.mult;
+      const long long lda = q.lda ? q.lda : K, ldb = q.ldb ? q.ldb : (opB == OP_N ? N : K);
+      auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+      const bool big = tm_mode == 2 || (K >= 256 && M * N >= 256 * 256);
+      if (big && al16(q.A) && al16(q.B) && lda % 2 == 0 && ldb % 2 == 0 && M > 0 && N > 0 && K > 0) {
+        CUtensorMap mapA, mapB;
+        const bool okA = tm_encode(&mapA, q.A, K, M, lda, 64);
+        const bool okB = opB == OP_N ? tm_encode(&mapB, q.B, N, K, ldb, 16) : tm_encode(&mapB, q.B, K, N, ldb, 64);
+        if (okA && okB) {
+          if (opB == OP_N) {
+            static const cudaError_t at = cudaFuncSetAttribute(gemm_tm_kernel<OP_N>,
+                                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);
+            if (at != cudaSuccess) return at;
+            gemm_tm_kernel<OP_N><<<grid, NTHREADS, TM_SMEM, s>>>(q, mapA, mapB, tiles_m, tiles_n);
+          } else {
+            static const cudaError_t at = cudaFuncSetAttribute(gemm_tm_kernel<OP_T>,
+                                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);
+            if (at != cudaSuccess) return at;
+            gemm_tm_kernel<OP_T><<<grid, NTHREADS, TM_SMEM, s>>>(q, mapA, mapB, tiles_m, tiles_n);
+          }
+          e = cudaGetLastError();
+          if (splits > 1) {
+            if (e == cudaSuccess) {
+              splitk_reduce_kernel<T><<<dim3((nmax + 255) / 256, mmax, chains), 256, 0, s>>>(q, splits);
+              e = cudaGetLastError();
+            }
+            cudaFreeAsync(q.ws, s);
+          }
+          return e;
+        }
+      }
+    }
+  }
   const bool tma = gemm_tma_ok<T>(q, opA, opB);
   switch (opA) {
     case OP_N: e = launch_b<T, OP_N>(q, opB, grid, tiles_m, tiles_n, tma, s); break;

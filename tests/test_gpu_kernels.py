@@ -63,8 +63,8 @@ for dtype in (np.float64, np.complex128):
     for opA in range(4):
         for opB in range(4):
             rng = np.random.default_rng(16 * opA + opB)
-            for (M, N, K) in [(128, 96, 192), (64, 190, 64), (200, 130, 256), (70, 66, 1024)]:
-                batch = 2
+            for (M, N, K, batch) in [(128, 96, 192, 2), (64, 190, 64, 2), (200, 130, 256, 1), (70, 66, 1024, 1),
+                                     (64, 64, 40, 1), (130, 258, 72, 1), (512, 320, 272, 1)]:
                 def rnd(*s):
                     x = rng.standard_normal(s)
                     return x + 1j * rng.standard_normal(s) if dtype == np.complex128 else x
@@ -81,13 +81,15 @@ print('TMA_GEMM_OK', worst)
 
 
 def test_gemm_tma_all_ops():
-    """The TMA-staged GEMM variant (bulk row copies + mbarrier pipeline) for every operand mode and both
-    dtypes (TTG_GEMM_TMA=2 routes all eligible products to it; by default only m-/n-contiguous operand
-    pairs use it), including split-K (K = 1024 with few tiles) and partial edge tiles."""
+    """The TMA-staged GEMM variants for every operand mode and both dtypes: bulk row copies + mbarrier
+    pipeline (TTG_GEMM_TMA=2 routes all eligible products to it; by default only m-/n-contiguous operand
+    pairs use it) and, for single-chain f64 products with A = N and B = N / T, the tensor-map kernel
+    (cp.async.bulk.tensor, swizzled tiles; TTG_GEMM_TM=2 lifts its size threshold), including split-K
+    (K = 1024 with few tiles), ragged K and partial edge tiles."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TTG_GEMM_TMA="2")
+    env = dict(os.environ, TTG_GEMM_TMA="2", TTG_GEMM_TM="2")
     r = subprocess.run([sys.executable, "-c", _TMA_SNIPPET], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "TMA_GEMM_OK" in r.stdout, r.stdout + r.stderr
