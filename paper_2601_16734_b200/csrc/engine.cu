@@ -233,6 +233,28 @@ struct Engine {
 
   int ub(DimExpr e) const { return e.idx < 0 ? e.mult : e.mult * bound[e.idx]; }
 
+  // Host mirror of the single chain's bond table (host_dims): refreshed once per sweep step (the sync the
+  // large split needs anyway), so the step's projection GEMMs X = L T, Y = X T, theta = Y R^T get host
+  // shapes and run on the tensor-map TMA kernel.  Entries written on the device since the last refresh
+  // are marked invalid and keep their device-side DimExpr.
+  bool host_dims = false;
+  std::vector<int> hostb;
+  std::vector<char> hostb_ok;
+  void refresh_bonds() {
+    if (!host_dims) return;
+    hostb.resize(ld);
+    CK(cudaMemcpyAsync(hostb.data(), d_bonds, ld * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    hostb_ok.assign(ld, 1);
+  }
+  void invalidate_bond(int idx) {
+    if (host_dims && idx >= 0 && idx < (int)hostb_ok.size()) hostb_ok[idx] = 0;
+  }
+  DimExpr resolve(DimExpr e) const {
+    if (host_dims && e.idx >= 0 && e.idx < (int)hostb_ok.size() && hostb_ok[e.idx]) return dconst(e.mult * hostb[e.idx]);
+    return e;
+  }
+
   // host copies of the bond table / chain states (profiling only)
   std::vector<int> hb;
   std::vector<ChainState> hs;
@@ -258,10 +280,12 @@ struct Engine {
           const double mk = a_upper ? (m <= kk ? m * kk - m * (m - 1) / 2.0 : kk * (kk + 1) / 2.0) : m * kk;
           flops += (Scalar<T>::is_complex ? 8.0 : 2.0) * mk * (double)N.eval(hb.data(), c, ld);
         }
-    GemmParams p{A, Bm, C, sA, sB, sC, M, N, K, d_bonds, ld, check_active ? d_state : nullptr, 1.0, beta};
+    // single chain with a host mirror: the chain is active whenever the sweep loop is running
+    GemmParams p{A,      Bm,   C,  sA, sB, sC, resolve(M), resolve(N), resolve(K),
+                 d_bonds, ld, (check_active && !host_dims) ? d_state : nullptr, 1.0, beta};
     p.a_upper = a_upper ? 1 : 0;
     ProfScope ps(ctx, TTG_PROF_GEMM, flops);
-    CK(gemm<T>(p, opA, opB, ub(M), ub(N), B, st, ub(K)));
+    CK(gemm<T>(p, opA, opB, ub(p.M), ub(p.N), B, st, ub(p.K)));
     ++ctx->launches;
   }
 
@@ -286,6 +310,17 @@ struct Engine {
   void S(const void* theta, long long s_theta, DimExpr M, DimExpr N, int out_idx, void* iso, long long s_iso,
          int mode, double tol, int max_bond, bool check_active, bool accumulate, void* work, long long s_work,
          const Warm& w = Warm(), bool no_pre = false) {
+    const DimExpr M_dev = M, N_dev = N;  // the split kernels read their shapes from the device table
+    (void)M_dev;
+    (void)N_dev;
+    struct Inval {  // the rank is written on the device: the host mirror of this bond is stale afterwards
+      Engine* e;
+      int idx;
+      ~Inval() {
+        e->invalidate_bond(idx);
+        e->invalidate_bond(e->pre_slot);
+      }
+    } inval{this, out_idx};
     SvdParams p{};
     static const int no_early = [] {
       const char* e = getenv("TTG_SVD_EARLY");
@@ -489,11 +524,17 @@ void Engine<T>::split_large(const void* theta, long long s_theta, DimExpr M, Dim
   (void)s_iso;
   std::vector<int> hb(ld);
   ChainState hs{};
-  CK(cudaMemcpyAsync(hb.data(), d_bonds, ld * sizeof(int), cudaMemcpyDeviceToHost, st));
-  if (check_active) CK(cudaMemcpyAsync(&hs, d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (check_active && !hs.active) return;
-  const int m = M.eval(hb.data(), 0, ld), n = N.eval(hb.data(), 0, ld);
+  const DimExpr Mr = resolve(M), Nr = resolve(N);
+  if (host_dims && Mr.idx < 0 && Nr.idx < 0) {
+    // shapes from the host mirror refreshed at the start of the sweep step (the chain is active there)
+  } else {
+    CK(cudaMemcpyAsync(hb.data(), d_bonds, ld * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (check_active) CK(cudaMemcpyAsync(&hs, d_state, sizeof(ChainState), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (check_active && !hs.active) return;
+  }
+  const int m = Mr.idx < 0 && host_dims ? Mr.mult : M.eval(hb.data(), 0, ld);
+  const int n = Nr.idx < 0 && host_dims ? Nr.mult : N.eval(hb.data(), 0, ld);
   const int l = mode == 0 ? m : n, k = mode == 0 ? n : m, r0 = std::min(l, k);
   const size_t es = sizeof(T);
   // TTG_PRE=2: the two-QR preconditioner below.  Default: one R-only QR (C4 A/B on one B200:
@@ -937,9 +978,17 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
     // ---- sweeps (simplify.hpp:66-91, 114-125)
     const int nsweeps = std::max(1, s.max_sweeps);
     std::vector<ChainState> hstate(B);
+    // host mirror of the bond table for one chain with large bonds (TTG_HOST_DIMS=0 disables): the sweep
+    // splits of such chains synchronise once per step anyway (split_large)
+    static const bool host_dims_env = [] {
+      const char* ev = getenv("TTG_HOST_DIMS");
+      return !(ev && ev[0] == '0');
+    }();
+    E.host_dims = host_dims_env && B == 1 && !Scalar<T>::is_complex && bound[L + 1] >= 256;
     for (int sw = 0; sw < nsweeps; ++sw) {
       for (int n = 0; n + 1 < L; ++n) {  // left to right
         const int dn = d[n], dn1 = d[n + 1];
+        E.refresh_bonds();
         E.G(lenv[n].p, P.env_cap[n], Ts(n), Tc(n), XZ.p, sxz, dbond(n), dconst(dn * t[n + 1]), dconst(t[n]), OP_N,
             OP_N, true);
         E.G(XZ.p, sxz, Ts(n + 1), Tc(n + 1), YW.p, syw, dbond(n, dn), dconst(dn1 * t[n + 2]), dconst(t[n + 1]),
@@ -967,6 +1016,7 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
       }
       for (int n = L - 2; n >= 0; --n) {  // right to left
         const int dn = d[n], dn1 = d[n + 1];
+        E.refresh_bonds();
         E.G(Ts(n + 1), Tc(n + 1), renv[n + 2].p, P.env_cap[n + 2], XZ.p, sxz, dconst(t[n + 1] * dn1), dbond(n + 2),
             dconst(t[n + 2]), OP_N, OP_T, true);
         E.G(Ts(n), Tc(n), XZ.p, sxz, YW.p, syw, dconst(t[n] * dn), dbond(n + 2, dn1), dconst(t[n + 1]), OP_N, OP_N,
