@@ -34,7 +34,10 @@ def check_against_reference(name, meta, tensors, ref_meta, ref_tensors):
         scale = max(nrm, ref_meta["error"])
         assert (abs(meta["error"] - ref_meta["error"]) <= 1e-10 * scale
                 or abs(meta["error"] ** 2 - ref_meta["error"] ** 2) <= 1e-13 * scale ** 2)
-        if "sweeps" in ref_meta and "sweeps" in meta:
+        # a target the ansatz holds exactly leaves dist^2 = <T,T> - |psi|^2 at cancellation level (eps <T,T>): whether
+        # sqrt(dist^2) <= 1e-12 |T| (simplify.hpp:118) then holds is decided by the last bit, so is the sweep count
+        exact_fit = ref_meta.get("residual", 1.0) ** 2 <= 1e-13 * scale ** 2
+        if "sweeps" in ref_meta and "sweeps" in meta and not exact_fit:
             assert meta["sweeps"] == ref_meta["sweeps"]
     assert distance(tensors, ref_tensors) <= 1e-10 * nrm
     if sum(int(np.log2(t.shape[1]) + 0.5) for t in ref_tensors) <= 16 and all(t.shape[1] == 2 for t in ref_tensors):
