@@ -86,3 +86,17 @@ def test_reference_random_uniform_mps_is_bit_exact():
                 got = O.loads_mps(f.read())
             want = O.random_uniform_mps(L, d, bond, seed)
             assert all(np.array_equal(x, y) for x, y in zip(got.tensors, want.tensors))
+
+
+@pytest.mark.parametrize("suite", ["core", "blas"])
+def test_reference_own_tests_pass_on_the_standin_build(suite):
+    """proj/tests/test_core.cpp and test_blas.cpp (the reference's tests for this path), compiled unchanged
+    against oracle/eigen_standin + oracle/catch2_standin: the stand-in build behaves as the reference expects."""
+    import os
+    import subprocess
+    exe = os.path.join(R.ROOT, "oracle", "_ref", "ref_test_" + suite)
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_test_%s not built (needs /root/reference)" % suite)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:]
+    assert r.stdout.strip().splitlines()[-1].startswith("ok:")
