@@ -285,7 +285,8 @@ def _roofline(prof, cfg_name=None):
     p = prof[dom]
     achieved = p["flops"] / (p["ms"] / 1e3) / 1e12 if p["ms"] > 0 else 0.0
     return {
-        "bound": "fp64",
+        "bound": "tensor",  # the FP64 tensor pipe (DMMA); on B200 the FP64 FMA pipe has the same peak
+        "pipe": "fp64 (DMMA m16n8k4 / DFMA)",
         "kernel": {"gemm": "ttg::gemm_kernel (DMMA m16n8k4)",
                    "svd": "ttg::" + (_SVD_TRAFFIC[cfg_name]["kernel"] if cfg_name in _SVD_TRAFFIC
                                      else "jacobi_svd_kernel"),

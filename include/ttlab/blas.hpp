@@ -19,11 +19,28 @@ inline CanonicalMPS apply(const MPO& op, const MPS& v, const Strategy& strategy 
   return gpu::canonical_from(o.h, 0);
 }
 
+/// blas.hpp:13-20.  The applied terms stay on the device: one MPO upload, `ttg_apply_raw` per term, then the
+/// sum is compressed by `ttg_simplify_sum` on the device handles (no host round trip of the expanded terms).
 inline CanonicalMPS apply(const MPO& op, const MPSSum& v, const Strategy& strategy = DEFAULT_STRATEGY) {
-  std::vector<MPS> applied;
-  applied.reserve(static_cast<size_t>(v.terms()));
-  for (const auto& s : v.states()) applied.push_back(detail::apply_raw(op, s));
-  return simplify(MPSSum(v.weights(), applied), strategy);
+  auto w = gpu::upload(op);
+  gpu::SumArgs a(v);
+  std::vector<gpu::DMps> applied;
+  std::vector<const ttg_dmps*> handles;
+  applied.reserve(static_cast<size_t>(a.n()));
+  for (int l = 0; l < a.n(); ++l) {
+    if (op.size() != v.states()[static_cast<size_t>(l)].size())
+      throw shape_error("apply: operator and state sizes differ");
+    ttg_dmps* t = nullptr;
+    gpu::check(gpu::ctx(), ttg_apply_raw(gpu::ctx(), w.h, a.handles[static_cast<size_t>(l)], &t));
+    applied.emplace_back(t);
+    handles.push_back(t);
+  }
+  const ttg_strategy s = gpu::to_c(strategy);
+  ttg_dmps* out = nullptr;
+  gpu::check(gpu::ctx(), ttg_simplify_sum(gpu::ctx(), a.n(), a.wr.data(), a.wi.data(), handles.data(), &s, nullptr,
+                                          &out, nullptr));
+  gpu::DMps o(out);
+  return gpu::canonical_from(o.h, 0);
 }
 
 inline CanonicalMPS apply(const MPOList& ops, const MPS& v, const Strategy& strategy = DEFAULT_STRATEGY) {
@@ -100,6 +117,96 @@ inline MPS hadamard(const MPS& u, const MPS& v) {
   double err = 0.0;
   auto ts = gpu::download(o.h, 0, &err, nullptr);
   return MPS(std::move(ts), err);
+}
+
+/// Register layout of a tensor product: A concatenates the registers, B interleaves them scale by scale
+/// (blas.hpp:140).
+enum class TensorOrder { A, B };
+
+namespace detail {
+/// Order B: output site (j, m) carries state m's tensor at scale j and the identity on the open bonds of the
+/// other states — those before m have already advanced to bond j + 1, those after m are still at bond j
+/// (blas.hpp:144-196).  The joint bond index is the mixed-radix number of the per-state indices, state 0
+/// most significant.
+inline MPS interleaved_product(const std::vector<MPS>& states) {
+  const index_t L = states.front().size(), M = static_cast<index_t>(states.size());
+  for (const auto& s : states)
+    if (s.size() != L) throw shape_error("order B requires states of equal length");
+  std::vector<Tensor3> out;
+  for (index_t j = 0; j < L; ++j)
+    for (index_t m = 0; m < M; ++m) {
+      std::vector<index_t> ld(static_cast<size_t>(M)), rd(static_cast<size_t>(M));
+      index_t left = 1, right = 1;
+      for (index_t k = 0; k < M; ++k) {
+        const Tensor3& t = states[static_cast<size_t>(k)][j];
+        ld[static_cast<size_t>(k)] = k < m ? t.right_dim() : t.left_dim();
+        rd[static_cast<size_t>(k)] = k <= m ? t.right_dim() : t.left_dim();
+        left *= ld[static_cast<size_t>(k)];
+        right *= rd[static_cast<size_t>(k)];
+      }
+      // strides of slot m and of the slots around it in the joint left / right index
+      index_t lo = 1;  // product of the dims of the slots after m (equal on both sides)
+      for (index_t k = m + 1; k < M; ++k) lo *= ld[static_cast<size_t>(k)];
+      index_t hi = 1;  // product of the dims of the slots before m (equal on both sides)
+      for (index_t k = 0; k < m; ++k) hi *= ld[static_cast<size_t>(k)];
+      const Tensor3& a = states[static_cast<size_t>(m)][j];
+      const index_t dl = a.left_dim(), dr = a.right_dim();
+      Tensor3 t(left, a.phys_dim(), right);
+      for (index_t h = 0; h < hi; ++h)
+        for (index_t x = 0; x < dl; ++x)
+          for (index_t y = 0; y < dr; ++y)
+            for (index_t s = 0; s < a.phys_dim(); ++s) {
+              const cplx v = a(x, s, y);
+              if (v == cplx(0)) continue;
+              for (index_t w = 0; w < lo; ++w) t((h * dl + x) * lo + w, s, (h * dr + y) * lo + w) = v;
+            }
+      out.push_back(std::move(t));
+    }
+  return MPS(std::move(out), 0.0);
+}
+}  // namespace detail
+
+/// Tensor product of several states (blas.hpp:200-216).  Exact host-side restructuring.
+inline MPS mps_tensor_product(const std::vector<MPS>& states, TensorOrder order = TensorOrder::A) {
+  if (states.empty()) throw shape_error("mps_tensor_product: no states");
+  double err = 0.0;
+  for (const auto& s : states) err += s.error();
+  if (order == TensorOrder::A) {
+    std::vector<Tensor3> out;
+    for (const auto& s : states)
+      for (index_t n = 0; n < s.size(); ++n) out.push_back(s[n]);
+    return MPS(std::move(out), err);
+  }
+  MPS out = detail::interleaved_product(states);
+  out.set_error(err);
+  return out;
+}
+
+/// Sum of mutually extended vectors: term k holds state k against all-ones registers for the others; the
+/// block sum is exact and built on the device by MPSSum::join (blas.hpp:220-246).
+inline MPS mps_tensor_sum(const std::vector<MPS>& states, TensorOrder order = TensorOrder::A) {
+  if (states.empty()) throw shape_error("mps_tensor_sum: no states");
+  const size_t M = states.size();
+  if (M == 1) return states.front();
+  std::vector<MPS> terms;
+  for (size_t k = 0; k < M; ++k) {
+    std::vector<MPS> factors;
+    for (size_t m = 0; m < M; ++m) {
+      if (m == k) {
+        factors.push_back(states[m]);
+        continue;
+      }
+      std::vector<Tensor3> ones;
+      for (index_t n = 0; n < states[m].size(); ++n) {
+        Tensor3 t(1, states[m][n].phys_dim(), 1);
+        std::fill(t.data(), t.data() + t.size(), cplx(1));
+        ones.push_back(std::move(t));
+      }
+      factors.emplace_back(std::move(ones), 0.0);
+    }
+    terms.push_back(mps_tensor_product(factors, order));
+  }
+  return MPSSum(std::vector<cplx>(M, cplx(1)), terms).join();
 }
 
 }  // namespace ttlab

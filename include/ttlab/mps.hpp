@@ -287,14 +287,69 @@ inline MPS basis_state(index_t L, index_t d, index_t idx) {
   return MPS(std::move(ts), 0.0);
 }
 
-inline MPS product_state(index_t L, const std::vector<cplx>& site) {
+/// Product state with the same single-site vector at every site (mps.hpp:517-528).
+inline MPS product_state(index_t L, const Vector& site) {
+  const index_t d = static_cast<index_t>(site.size());
   std::vector<Tensor3> ts;
   for (index_t n = 0; n < L; ++n) {
-    Tensor3 t(1, static_cast<index_t>(site.size()), 1);
-    for (size_t s = 0; s < site.size(); ++s) t(0, static_cast<index_t>(s), 0) = site[s];
+    Tensor3 t(1, d, 1);
+    for (index_t s = 0; s < d; ++s) t(0, s, 0) = site[s];
     ts.push_back(std::move(t));
   }
   return MPS(std::move(ts), 0.0);
 }
 
+/// Dense vector -> CanonicalMPS at centre 0 (mps.hpp:453-486): the index is split per `dims` (most
+/// significant first) by right-to-left truncated splits (device `schmidt_split`), whose errors are mutually
+/// orthogonal; ledger = sqrt(sum err^2) + fp_error_floor(|v|).
+inline CanonicalMPS mps_from_dense(const Vector& v, const std::vector<index_t>& dims,
+                                   const Strategy& strategy = DEFAULT_STRATEGY) {
+  index_t total = 1;
+  for (index_t d : dims) {
+    if (d < 1) throw shape_error("mps_from_dense: physical dimensions must be >= 1");
+    total *= d;
+  }
+  const index_t nv = static_cast<index_t>(v.size());
+  if (total != nv) throw shape_error("mps_from_dense: vector length does not match dimensions");
+  const index_t L = static_cast<index_t>(dims.size());
+  std::vector<Tensor3> ts(static_cast<size_t>(L));
+  std::vector<cplx> rest(static_cast<size_t>(nv));  // row-major (rows x cols) remainder, rows * cols = rest.size()
+  double vnorm2 = 0.0;
+  for (index_t i = 0; i < nv; ++i) {
+    rest[static_cast<size_t>(i)] = v[i];
+    vnorm2 += std::norm(rest[static_cast<size_t>(i)]);
+  }
+  double err2 = 0.0;
+  index_t right = 1;
+  for (index_t n = L - 1; n > 0; --n) {
+    const index_t d = dims[static_cast<size_t>(n)], cols = d * right;
+    const index_t rows = static_cast<index_t>(rest.size()) / cols;
+    Matrix theta(rows, cols);
+    for (index_t i = 0; i < rows; ++i)
+      for (index_t j = 0; j < cols; ++j) theta(i, j) = rest[static_cast<size_t>(i * cols + j)];
+    const SchmidtSplit sp = schmidt_split(theta, strategy, SweepDirection::RIGHT_TO_LEFT);
+    err2 += sp.error * sp.error;
+    const index_t rank = sp.b.rows();
+    Tensor3 t(rank, d, right);
+    for (index_t i = 0; i < rank; ++i)
+      for (index_t j = 0; j < cols; ++j) t.data()[i * cols + j] = sp.b(i, j);
+    ts[static_cast<size_t>(n)] = std::move(t);
+    rest.assign(static_cast<size_t>(rows * rank), cplx(0));
+    for (index_t i = 0; i < rows; ++i)
+      for (index_t j = 0; j < rank; ++j) rest[static_cast<size_t>(i * rank + j)] = sp.a(i, j);
+    right = rank;
+  }
+  Tensor3 first(1, dims[0], right);
+  std::copy(rest.begin(), rest.end(), first.data());
+  ts[0] = std::move(first);
+  MPS out(std::move(ts), std::sqrt(err2) + detail::fp_error_floor(std::sqrt(vnorm2)));
+  CanonicalMPS result(out, 0, NO_TRUNCATION);
+  result.set_error(out.error());
+  if (strategy.normalize) result.normalize_in_place();
+  return result;
+}
+
 }  // namespace ttlab
+
+// the device definitions (ttlab/gpu.hpp, pulled in at the end of mpo.hpp) need the MPO container
+#include "ttlab/mpo.hpp"

@@ -5,6 +5,7 @@
 
 #include <optional>
 
+#include "ttlab/forms.hpp"
 #include "ttlab/gpu.hpp"
 
 namespace ttlab {
@@ -44,6 +45,38 @@ inline CanonicalMPS combine(const std::vector<cplx>& weights, const std::vector<
   for (const auto& s : states)
     if (s.physical_dimensions() != dims) throw shape_error("combine: states must share physical dimensions");
   return simplify(MPSSum(weights, states), strategy);
+}
+
+namespace detail {
+/// MPO -> MPS with the (out, in) pair fused into one physical index, and back (simplify.hpp:219-237).
+inline MPS flatten_mpo(const MPO& op) {
+  std::vector<Tensor3> ts;
+  for (index_t n = 0; n < op.size(); ++n) ts.push_back(op[n].fuse_physical());
+  return MPS(std::move(ts), 0.0);
+}
+inline MPO unflatten_mpo(const MPS& state, const std::vector<index_t>& out_dims, const std::vector<index_t>& in_dims) {
+  std::vector<Tensor4> ts;
+  for (index_t n = 0; n < state.size(); ++n)
+    ts.push_back(Tensor4::split_physical(state[n], out_dims[static_cast<size_t>(n)], in_dims[static_cast<size_t>(n)]));
+  return MPO(std::move(ts));
+}
+}  // namespace detail
+
+/// Compress an MPO: flatten, simplify the state on the device, unflatten (simplify.hpp:241-245).
+inline MPO simplify_mpo(const MPO& op, const Strategy& strategy = DEFAULT_STRATEGY) {
+  const CanonicalMPS compact = simplify(detail::flatten_mpo(op), strategy.with_normalize(false));
+  return detail::unflatten_mpo(compact, op.out_dimensions(), op.in_dimensions());
+}
+
+/// Compress a weighted sum of MPOs the same way (simplify.hpp:248-260).
+inline MPO simplify_mpo(const std::vector<cplx>& weights, const std::vector<MPO>& terms,
+                        const Strategy& strategy = DEFAULT_STRATEGY) {
+  if (weights.empty() || weights.size() != terms.size())
+    throw shape_error("simplify_mpo: weights and terms must be non-empty and match");
+  std::vector<MPS> flats;
+  for (const auto& t : terms) flats.push_back(detail::flatten_mpo(t));
+  const CanonicalMPS compact = simplify(MPSSum(weights, flats), strategy.with_normalize(false));
+  return detail::unflatten_mpo(compact, terms.front().out_dimensions(), terms.front().in_dimensions());
 }
 
 /// Batched simplify of independent, identically shaped chains (one device call).

@@ -25,3 +25,19 @@ def test_dropin_headers_compile_without_eigen():
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Iinclude", "tests/cpp/test_dropin.cpp"], cwd=ROOT,
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["test_core", "test_blas"])
+def test_reference_own_tests_through_the_dropin_headers(suite):
+    """proj/tests/test_core.cpp / test_blas.cpp of the reference, compiled UNCHANGED against include/ttlab
+    (+ the Eigen / Catch2 stand-ins of oracle/) and linked with libttgpu.so: every split, canonicalization,
+    simplify, apply, scprod and expectation in them runs on the B200.  Built by __graft_entry__.build() where
+    /root/reference exists; the binaries travel with the snapshot."""
+    exe = os.path.join(ROOT, "tests", "cpp", "ref_" + suite)
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/ref_%s not built (needs /root/reference at build time)" % suite)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1].startswith("ok:")

@@ -177,6 +177,7 @@ def test_jacobi_svd_random(dtype, shape, mode, svd_impl):
 
 
 @pytest.mark.parametrize("dtype,shape", [(np.float64, (600, 520)), (np.float64, (1000, 700)), (np.float64, (1024, 1024)),
+                                         (np.float64, (1536, 1536)), (np.float64, (2048, 1100)),
                                          (np.complex128, (480, 300)), (np.complex128, (300, 480))])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_jacobi_svd_grid_large(dtype, shape, mode, monkeypatch):
