@@ -178,7 +178,8 @@ def test_jacobi_svd_random(dtype, shape, mode, svd_impl):
 
 @pytest.mark.parametrize("dtype,shape", [(np.float64, (600, 520)), (np.float64, (1000, 700)), (np.float64, (1024, 1024)),
                                          (np.float64, (1536, 1536)), (np.float64, (2048, 1100)),
-                                         (np.complex128, (480, 300)), (np.complex128, (300, 480))])
+                                         (np.complex128, (480, 300)), (np.complex128, (300, 480)),
+                                         (np.complex128, (1000, 520))])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_jacobi_svd_grid_large(dtype, shape, mode, monkeypatch):
     """Grid-cooperative block Jacobi at the C3/C4 split sizes (rows split over 2-CTA clusters)."""

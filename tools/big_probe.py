@@ -12,7 +12,8 @@ from paper_2601_16734_b200 import ttlab  # noqa: E402
 from tests._compare import distance  # noqa: E402
 
 n, chi, out = (int(a) for a in (sys.argv[1:4] if len(sys.argv) > 3 else (22, 1024, 768)))
-psi = I.random_mps(n, 2, chi, 777)
+cplx = len(sys.argv) > 4 and sys.argv[4] == "c"  # complex128 chain (splits beyond 512 rows: warp-pair kernel, E = 32)
+psi = I.random_mps(n, 2, chi, 777, complex_=cplx)
 strat = dict(max_bond=out, max_sweeps=1)
 rep = []
 t0 = time.time()
