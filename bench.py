@@ -311,10 +311,33 @@ def _need_gpus(torch, world):
                          f"found {torch.cuda.device_count() if torch.cuda.is_available() else 0}; no CPU fallback")
 
 
+def _context_comm(ctx, torch, dist, rank, world):
+    """Give the library context its NCCL communicator (ttg_comm_init; id shipped by torch.distributed) and
+    agree over the ranks whether every one got it; otherwise the stats collective goes through
+    torch.distributed's NCCL all-gather."""
+    if world == 1:
+        return True
+    n, _ = ctx.comm_info()
+    ok = 1
+    if n != world:
+        try:
+            from paper_2601_16734_b200.batch import init_context_comm
+            init_context_comm(ctx, world, rank)
+        except Exception as e:  # noqa: BLE001 - reported, then the torch collective is used on every rank
+            print(f"bench.py[rank {rank}]: context communicator unavailable ({e}); using torch.distributed",
+                  file=sys.stderr)
+            ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(flag.item())
+
+
 def c5_scaling(ttlab, torch, dist, ctx, stream, rank, world, steps=3):
     """Config 5 (1024 chains, chi 128 -> 64) sharded over the ranks: chains/s at
     this N and T1/(N T_N), T1 timed on rank 0 with the whole batch."""
-    from paper_2601_16734_b200.batch import gather_chain_stats
+    import numpy as np
+    from paper_2601_16734_b200.batch import gather_chain_stats, gather_chain_stats_ctx
+    native = _context_comm(ctx, torch, dist, rank, world)
     cfg, chains, _ = workload("C5", rank, world)
     total = cfg.batch
     strat = ttlab.Strategy(max_bond=cfg.out_chi, tolerance=cfg.tolerance, max_sweeps=cfg.max_sweeps)
@@ -329,10 +352,15 @@ def c5_scaling(ttlab, torch, dist, ctx, stream, rank, world, steps=3):
         for _ in range(nsteps):
             reps = []
             ttlab.simplify(batch, strat, report=reps)
-            st = torch.tensor([[r["norm"], r["error"], float(r["sweeps"])] for r in reps], dtype=torch.float64,
-                              device=dev)
-            allst = gather_chain_stats(st, total, world) if collective else st
-            sweeps += int(allst[:, 2].sum().item())
+            if native:  # the collective on the communicator the library context owns (ttg_comm_allgather_f64)
+                st = np.array([[r["norm"], r["error"], float(r["sweeps"])] for r in reps])
+                allst = gather_chain_stats_ctx(ctx, st, total, world) if collective else st
+                sweeps += int(allst[:, 2].sum())
+            else:
+                st = torch.tensor([[r["norm"], r["error"], float(r["sweeps"])] for r in reps], dtype=torch.float64,
+                                  device=dev)
+                allst = gather_chain_stats(st, total, world) if collective else st
+                sweeps += int(allst[:, 2].sum().item())
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / nsteps, sweeps / nsteps
@@ -360,6 +388,8 @@ def c5_scaling(ttlab, torch, dist, ctx, stream, rank, world, steps=3):
                         "NCCL all-gather of per-chain (norm, error, sweeps) per batch",
             "n_gpus": world, "ms_per_batch": t_n, "chains_per_s": total / (t_n / 1e3),
             "sweeps_per_batch": sweeps, "t1_ms_per_batch": t_1, "efficiency_t1_over_n_tn": t_1 / (world * t_n),
+            "collective": ("ttg_comm_allgather_f64 on the context's own NCCL communicator" if native
+                           else "torch.distributed all_gather_into_tensor (NCCL)"),
             "steps": steps}
 
 

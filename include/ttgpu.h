@@ -102,6 +102,23 @@ ttg_status ttg_synchronize(ttg_ctx* ctx);
 int64_t ttg_kernel_launches(const ttg_ctx* ctx);
 const char* ttg_version(void);
 
+/* ---- communicator (batched configs, one rank per GPU) --------------------------
+ * The reference has no multi-process path; its batched use is a host loop over simplify
+ * (simplify.hpp:182-195).  Here independent chains are sharded over ranks with no exchange during the
+ * sweeps, and the context owns the NCCL communicator for the one collective of a batch: the all-gather
+ * of per-chain scalars (norm, error, sweeps).  libnccl.so.2 is bound at run time (TTG_NCCL_LIB overrides
+ * the name); contexts without a communicator behave as a world of one.
+ *   rank 0: ttg_comm_unique_id -> ship the TTG_COMM_ID_BYTES to every rank by the host's own means
+ *   every rank: ttg_comm_init(ctx, nranks, rank, id)      (collective: ncclCommInitRank on ctx's device)
+ *   ttg_comm_allgather_f64: send[count] of every rank -> recv[nranks * count] in rank order, host
+ *   buffers, on the context stream, synchronous at return. */
+#define TTG_COMM_ID_BYTES 128
+ttg_status ttg_comm_unique_id(ttg_ctx* ctx, void* id /* TTG_COMM_ID_BYTES */);
+ttg_status ttg_comm_init(ttg_ctx* ctx, int nranks, int rank, const void* id);
+ttg_status ttg_comm_info(const ttg_ctx* ctx, int* nranks, int* rank);
+ttg_status ttg_comm_allgather_f64(ttg_ctx* ctx, const double* send, int64_t count, double* recv);
+ttg_status ttg_comm_free(ttg_ctx* ctx);
+
 /* Per-kernel-class timing: when enabled, every launch is bracketed by CUDA
  * events on the context stream and GEMM/SVD/QR launches record their executed
  * flops (read from the device bond table, one host sync per launch: use a

@@ -45,6 +45,11 @@ SIGNATURES = {
     "ttg_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ttg_synchronize": (C.c_int, [C.c_void_p]),
     "ttg_kernel_launches": (C.c_int64, [C.c_void_p]),
+    "ttg_comm_unique_id": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ttg_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ttg_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ttg_comm_allgather_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "ttg_comm_free": (C.c_int, [C.c_void_p]),
     "ttg_version": (C.c_char_p, []),
     "ttg_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "ttg_profile_svd_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),

@@ -23,6 +23,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: the library is bound with dlopen (ttg_comm_*)
+
 #include "../../include/ttgpu.h"
 #include "common.cuh"
 #include "gemm.cuh"
@@ -58,6 +61,9 @@ struct ttg_ctx {
   // pinned double buffer of the TTLAB1 file I/O (allocated on first use)
   void* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // NCCL communicator of the batched configs (one rank per GPU), see ttg_comm_init
+  void* comm = nullptr;
+  int comm_rank = 0, comm_size = 1;
   void flush_profile() {
     if (pending.empty()) return;
     cudaStreamSynchronize(stream);
@@ -1274,6 +1280,7 @@ ttg_status ttg_create(int device, ttg_ctx** out) {
 void ttg_destroy(ttg_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
+  ttg_comm_free(ctx);
   ctx->flush_profile();
   if (ctx->d_sweeps) cudaFree(ctx->d_sweeps);
   for (int i = 0; i < 2; ++i) {
@@ -1282,6 +1289,122 @@ void ttg_destroy(ttg_ctx* ctx) {
   }
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL communicator owned by the context.  The batched configs shard independent
+// chains over one rank per GPU; the only exchange is one all-gather of per-chain scalars per batch.
+// libnccl is bound at run time (dlopen by soname: inside a torch process that is torch's own copy), so
+// single-GPU users never need it and the library has no link-time dependency on it.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  void* handle = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  std::string why;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    const char* env = getenv("TTG_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n || !*n) continue;
+      a.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (a.handle) break;
+    }
+    if (!a.handle) {
+      a.why = "libnccl.so.2 not found (set TTG_NCCL_LIB)";
+      return a;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.handle, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.handle, "ncclCommInitRank"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.handle, "ncclAllGather"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.handle, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.handle, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.AllGather || !a.CommDestroy || !a.GetErrorString) {
+      a.why = "libnccl lacks a required symbol";
+      a.handle = nullptr;
+    }
+    return a;
+  }();
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error{TTG_CUDA, std::string(what) + ": " + nccl_api().GetErrorString(r)};
+}
+NcclApi& nccl_required() {
+  NcclApi& a = nccl_api();
+  if (!a.handle) throw Error{TTG_CUDA, "NCCL unavailable: " + a.why};
+  return a;
+}
+}  // namespace
+
+static_assert(sizeof(ncclUniqueId) == TTG_COMM_ID_BYTES, "ttgpu.h: TTG_COMM_ID_BYTES must match ncclUniqueId");
+
+ttg_status ttg_comm_unique_id(ttg_ctx* ctx, void* id) {
+  return guarded(ctx, [&] {
+    if (!id) throw Error{TTG_INVALID, "ttg_comm_unique_id: null id"};
+    ncclUniqueId u;
+    nccl_check(nccl_required().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+ttg_status ttg_comm_init(ttg_ctx* ctx, int nranks, int rank, const void* id) {
+  return guarded(ctx, [&] {
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) throw Error{TTG_INVALID, "ttg_comm_init: bad rank / size / id"};
+    if (ctx->comm) throw Error{TTG_INVALID, "ttg_comm_init: the context already owns a communicator"};
+    CK(cudaSetDevice(ctx->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    ncclComm_t c = nullptr;
+    nccl_check(nccl_required().CommInitRank(&c, nranks, u, rank), "ncclCommInitRank");
+    ctx->comm = c;
+    ctx->comm_rank = rank;
+    ctx->comm_size = nranks;
+  });
+}
+
+ttg_status ttg_comm_info(const ttg_ctx* ctx, int* nranks, int* rank) {
+  if (!ctx) return TTG_INVALID;
+  if (nranks) *nranks = ctx->comm ? ctx->comm_size : 1;
+  if (rank) *rank = ctx->comm ? ctx->comm_rank : 0;
+  return TTG_OK;
+}
+
+ttg_status ttg_comm_allgather_f64(ttg_ctx* ctx, const double* send, int64_t count, double* recv) {
+  return guarded(ctx, [&] {
+    if (count < 0 || (count > 0 && (!send || !recv))) throw Error{TTG_INVALID, "ttg_comm_allgather_f64: bad arguments"};
+    if (count == 0) return;
+    if (!ctx->comm) {  // no communicator: a world of one
+      std::memcpy(recv, send, (size_t)count * sizeof(double));
+      return;
+    }
+    CK(cudaSetDevice(ctx->device));
+    const size_t nb = (size_t)count * sizeof(double);
+    DevBuf ds(nb, ctx->stream), dr(nb * ctx->comm_size, ctx->stream);
+    CK(cudaMemcpyAsync(ds.p, send, nb, cudaMemcpyHostToDevice, ctx->stream));
+    nccl_check(nccl_api().AllGather(ds.p, dr.p, (size_t)count, ncclFloat64, static_cast<ncclComm_t>(ctx->comm), ctx->stream),
+               "ncclAllGather");
+    CK(cudaMemcpyAsync(recv, dr.p, nb * ctx->comm_size, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+ttg_status ttg_comm_free(ttg_ctx* ctx) {
+  if (!ctx) return TTG_INVALID;
+  if (ctx->comm) {
+    nccl_api().CommDestroy(static_cast<ncclComm_t>(ctx->comm));
+    ctx->comm = nullptr;
+    ctx->comm_rank = 0;
+    ctx->comm_size = 1;
+  }
+  return TTG_OK;
 }
 
 const char* ttg_last_error(const ttg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

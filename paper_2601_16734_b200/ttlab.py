@@ -130,6 +130,38 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib.ttg_kernel_launches(self.handle))
 
+    # ---- NCCL communicator owned by the context (batched configs) ----
+    COMM_ID_BYTES = 128
+
+    def comm_unique_id(self) -> bytes:
+        """Rank 0: a fresh communicator id to ship to every rank (ncclGetUniqueId)."""
+        buf = C.create_string_buffer(self.COMM_ID_BYTES)
+        self.check(lib.ttg_comm_unique_id(self.handle, buf))
+        return buf.raw
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Collective over all ranks: the context joins the communicator `uid` (ncclCommInitRank)."""
+        if len(uid) != self.COMM_ID_BYTES:
+            raise ShapeError("comm_init: the id must be COMM_ID_BYTES long")
+        self.check(lib.ttg_comm_init(self.handle, int(nranks), int(rank), C.create_string_buffer(uid, len(uid))))
+
+    def comm_info(self):
+        n, r = C.c_int(), C.c_int()
+        self.check(lib.ttg_comm_info(self.handle, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
+    def allgather_f64(self, send: np.ndarray) -> np.ndarray:
+        """send[count] of every rank -> (nranks, count) in rank order (ncclAllGather on the context stream)."""
+        send = np.ascontiguousarray(send, dtype=np.float64).ravel()
+        n, _ = self.comm_info()
+        recv = np.empty((n, send.size), dtype=np.float64)
+        self.check(lib.ttg_comm_allgather_f64(self.handle, C.c_void_p(send.ctypes.data), send.size,
+                                              C.c_void_p(recv.ctypes.data)))
+        return recv
+
+    def comm_free(self):
+        self.check(lib.ttg_comm_free(self.handle))
+
     PROFILE_CLASSES = {"gemm": 0, "svd": 1, "qr": 2, "expand": 3}
 
     def profile_enable(self, on: bool = True):

@@ -128,6 +128,21 @@ int main() {
       CHECK(dist(mps_to_dense(batch[i]), mps_to_dense(one)) < 1e-10);
       CHECK(std::abs(batch[i].error() - one.error()) < 1e-12);
     }
+    // sharded form on the context's communicator: one GPU here, so a world of one, first
+    // without a communicator, then on a single-rank NCCL communicator (ncclCommInitRank + ncclAllGather)
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) gpu::comm_init(1, 0, gpu::comm_unique_id());
+      BatchStats all;
+      auto sharded = simplify_batch(chains, strat, &all, 4);
+      CHECK(all.norm.size() == 4 && all.error.size() == 4 && all.sweeps.size() == 4);
+      for (int i = 0; i < 4; ++i) {
+        CHECK(std::abs(all.norm[static_cast<size_t>(i)] - batch[i].norm()) < 1e-12 * batch[i].norm());
+        CHECK(std::abs(all.error[static_cast<size_t>(i)] - batch[i].error()) < 1e-12);
+        CHECK(all.sweeps[static_cast<size_t>(i)] >= 1);
+      }
+    }
+    CHECK(gpu::shard_range(1024, 8, 3).first == 384 && gpu::shard_range(1024, 8, 3).second == 512);
+    CHECK(gpu::shard_range(10, 4, 1).first == 3 && gpu::shard_range(10, 4, 3).second == 10);
   });
   section("combine: v+v, v-v, 3-term dense sum, SVD route, errors (test_blas.cpp:8-36)", [] {
     MPS v = random_uniform_mps(4, 2, 2, 1);

@@ -131,3 +131,27 @@ def test_batch_upload_download_staged():
                 assert a.shape == b.shape and np.array_equal(a, b)
             for a, b in zip(d.to_tensors(c), g):
                 assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_context_communicator_world_of_one():
+    """ttg_comm_*: the context owns the NCCL communicator of the batched configs.  One GPU here:
+    a single-rank communicator must initialise (ncclCommInitRank through the run-time binding of libnccl) and
+    the all-gather must return the local rows; without a communicator the context is a world of one."""
+    from paper_2601_16734_b200 import ttlab
+    from paper_2601_16734_b200.batch import gather_chain_stats_ctx
+    ctx = ttlab.Context(0)
+    assert ctx.comm_info() == (1, 0)
+    x = np.arange(12, dtype=np.float64) * 0.5
+    assert np.array_equal(ctx.allgather_f64(x), x.reshape(1, -1))
+    uid = ctx.comm_unique_id()
+    assert len(uid) == ttlab.Context.COMM_ID_BYTES and any(uid)
+    ctx.comm_init(1, 0, uid)
+    assert ctx.comm_info() == (1, 0)
+    assert np.array_equal(ctx.allgather_f64(x), x.reshape(1, -1))
+    with pytest.raises(Exception):
+        ctx.comm_init(1, 0, uid)  # already owns one
+    rows = np.arange(15, dtype=np.float64).reshape(5, 3)
+    assert np.array_equal(gather_chain_stats_ctx(ctx, rows, 5, 1), rows)
+    ctx.comm_free()
+    assert ctx.comm_info() == (1, 0)
