@@ -16,6 +16,8 @@
 //          apply_sum    <mpo> <n> <w_re> <w_im> <mps> ...   apply(MPO, MPSSum) blas.hpp:13-20
 //          scprod       <mps> <mps>            ttlab::scprod           mps.hpp:416-423
 //          expectation_mpo <mpo> <mps> <mps>   blas.hpp:128-138
+//          qft | iqft   <mps>                  ttlab::qft / iqft (apply(MPOList)) qft.hpp:108-113, blas.hpp:24-32
+//          qft_flip     <mps>                  ttlab::qft_flip         qft.hpp:117-128
 //          random_uniform <L> <d> <bond> <seed>  random_uniform_mps   mps.hpp:488-513
 //     strategy = method:tolerance:simplification_tolerance:max_bond:max_sweeps:normalize
 //                (method V|S, max_bond 0 = unbounded)
@@ -27,6 +29,7 @@
 #include <vector>
 
 #include "ttlab/blas.hpp"
+#include "ttlab/qft.hpp"
 #include "ttlab/serialize.hpp"
 
 using namespace ttlab;
@@ -131,6 +134,15 @@ int main(int argc, char **argv) {
     } else if (op == "expectation_mpo") {
       const cplx v = expectation_mpo(load_mpo(arg(0)), load_mps(arg(1)), load_mps(arg(2)));
       std::printf("{\"re\": %.17g, \"im\": %.17g}\n", v.real(), v.imag());
+    } else if (op == "qft" || op == "iqft") {
+      MPS v = load_mps(arg(0));
+      CanonicalMPS out = op == "qft" ? qft(v, strat) : iqft(v, strat);
+      save_mps(outp, out);
+      report(out, "");
+    } else if (op == "qft_flip") {
+      MPS out = qft_flip(load_mps(arg(0)));
+      save_mps(outp, out);
+      report(out, "");
     } else if (op == "random_uniform") {
       MPS out = random_uniform_mps(std::atoll(arg(0).c_str()), std::atoll(arg(1).c_str()),
                                    std::atoll(arg(2).c_str()), std::strtoull(arg(3).c_str(), nullptr, 10));

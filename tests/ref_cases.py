@@ -110,6 +110,10 @@ CASES = {
     "apply_sum_2terms": ("apply_sum", strat(max_bond=8),
                          lambda: dict(mpo=I.laplacian_mpo(8), mps=[I.random_mps(8, 2, 4, 51), I.random_mps(8, 2, 6, 52)],
                                       weights=[1.0 + 0j, 2.0 + 0j])),
+    # --- MPO lists: the Fourier transform circuit (qft.hpp:68-113 through apply(MPOList), blas.hpp:24-32)
+    "qft_uniform_n8": ("qft", strat(), lambda: dict(mps=[_ru(8, 2, 4, 71)])),
+    "iqft_complex_n10_chi8": ("iqft", strat(max_bond=8), lambda: dict(mps=[I.random_mps(10, 2, 8, 72, complex_=True)])),
+    "qft_product_state_n12": ("qft", strat(tolerance=1e-10), lambda: dict(mps=[_ru(12, 2, 1, 73)])),
     # --- scalars (mps.hpp:416-423, blas.hpp:128-138)
     "scprod_uniform": ("scprod", strat(), lambda: dict(mps=[_ru(9, 2, 5, 61), _ru(9, 2, 7, 62)])),
     "expectation_local_sum": ("expectation_mpo", strat(),
@@ -209,6 +213,15 @@ def load_fixture():
     return out
 
 
+def _qft_layers_host(L, inverse):
+    """The circuit layers as host tensors (paper_2601_16734_b200/qft.py builds them on the host; they are
+    checked against the oracle's dense circuit in tests/test_qft_host.py)."""
+    from paper_2601_16734_b200 import qft as Q
+    sign = 1.0 if inverse else -1.0
+    order = range(L) if inverse else range(L - 1, -1, -1)  # qft.hpp:84-100: matrix order, last factor acts first
+    return [Q.qft_layer(L, list(range(L)), m, sign, inverse) for m in order]
+
+
 # ----------------------------------------------------------------------------- oracle runs
 def run_oracle(name):
     """The oracle restatement on the same case: (meta, tensors)."""
@@ -228,6 +241,11 @@ def run_oracle(name):
         out = O.simplify_sum(O.MPSSum(inp["weights"], [_omps(t) for t in inp["mps"]]), s)
     elif op == "apply_sum":
         out = O.apply_sum(O.MPO(inp["mpo"]), O.MPSSum(inp["weights"], [_omps(t) for t in inp["mps"]]), s)
+    elif op in ("qft", "iqft"):
+        layers = _qft_layers_host(len(inp["mps"][0]), op == "iqft")
+        out = _omps(inp["mps"][0])
+        for layer in reversed(layers):  # the last factor acts first (blas.hpp:24-32)
+            out = O.apply(O.MPO(layer), out, s)
     elif op == "scprod":
         v = O.scprod(_omps(inp["mps"][0]), _omps(inp["mps"][1]))
         return {"re": float(np.real(v)), "im": float(np.imag(v))}, None

@@ -31,6 +31,9 @@ def run_gpu(name):
         out = t.simplify(t.MPSSum(inp["weights"], inp["mps"]), s, report=rep)
     elif op == "apply_sum":
         out = t.apply(inp["mpo"], t.MPSSum(inp["weights"], inp["mps"]), s, report=rep)
+    elif op in ("qft", "iqft"):
+        from paper_2601_16734_b200 import qft as Q
+        out = (Q.qft if op == "qft" else Q.iqft)(inp["mps"][0], s)
     elif op == "scprod":
         v = complex(t.scprod(inp["mps"][0], inp["mps"][1])[0])
         return {"re": v.real, "im": v.imag}, None

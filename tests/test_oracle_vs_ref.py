@@ -32,8 +32,12 @@ def check_against_reference(name, meta, tensors, ref_meta, ref_tensors):
     if name not in ROUNDING_LEVEL:
         # the ledger holds residual + carried errors; residual^2 = <T,T> - |psi|^2 cancels at eps <T,T>
         scale = max(nrm, ref_meta["error"])
+        # MPO lists (qft / iqft) add one residual per layer to the ledger (blas.hpp:24-32); every layer the bond
+        # limit holds exactly contributes sqrt of a cancellation-level dist^2, i.e. noise of order sqrt(eps) |T|
+        layers = len(ref_tensors) if R.CASES[name][0] in ("qft", "iqft") else 0
         assert (abs(meta["error"] - ref_meta["error"]) <= 1e-10 * scale
-                or abs(meta["error"] ** 2 - ref_meta["error"] ** 2) <= 1e-13 * scale ** 2)
+                or abs(meta["error"] ** 2 - ref_meta["error"] ** 2) <= 1e-13 * scale ** 2
+                or abs(meta["error"] - ref_meta["error"]) <= layers * 3.2e-7 * scale)
         # a target the ansatz holds exactly leaves dist^2 = <T,T> - |psi|^2 at cancellation level (eps <T,T>): whether
         # sqrt(dist^2) <= 1e-12 |T| (simplify.hpp:118) then holds is decided by the last bit, so is the sweep count
         exact_fit = ref_meta.get("residual", 1.0) ** 2 <= 1e-13 * scale ** 2
