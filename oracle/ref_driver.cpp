@@ -18,6 +18,10 @@
 //          expectation_mpo <mpo> <mps> <mps>   blas.hpp:128-138
 //          qft | iqft   <mps>                  ttlab::qft / iqft (apply(MPOList)) qft.hpp:108-113, blas.hpp:24-32
 //          qft_flip     <mps>                  ttlab::qft_flip         qft.hpp:117-128
+//          heff <mpo> <bra> <ket> <site>       operator environments (environments.hpp:42-83) up to the pair
+//                                              (site, site+1) and y = H_eff x for x = join_pair(ket pair)
+//                                              (detail::apply_effective_two_site, eigensolvers.hpp:15-64);
+//                                              <out> receives y as raw complex128
 //          random_uniform <L> <d> <bond> <seed>  random_uniform_mps   mps.hpp:488-513
 //     strategy = method:tolerance:simplification_tolerance:max_bond:max_sweeps:normalize
 //                (method V|S, max_bond 0 = unbounded)
@@ -29,6 +33,7 @@
 #include <vector>
 
 #include "ttlab/blas.hpp"
+#include "ttlab/eigensolvers.hpp"
 #include "ttlab/qft.hpp"
 #include "ttlab/serialize.hpp"
 
@@ -143,6 +148,25 @@ int main(int argc, char **argv) {
       MPS out = qft_flip(load_mps(arg(0)));
       save_mps(outp, out);
       report(out, "");
+    } else if (op == "heff") {
+      const MPO W = load_mpo(arg(0));
+      const MPS bra = load_mps(arg(1)), ket = load_mps(arg(2));
+      const index_t site = std::atoll(arg(3).c_str());
+      detail::OpEnv lenv = detail::begin_op_environment(), renv = detail::begin_op_environment();
+      for (index_t n = 0; n < site; ++n)
+        lenv = detail::update_left_op_environment(lenv, bra[n], W[n], ket[n]);
+      for (index_t n = ket.size() - 1; n > site + 1; --n)
+        renv = detail::update_right_op_environment(renv, bra[n], W[n], ket[n]);
+      const Vector x = detail::tensor_to_vector(detail::join_pair(ket[site], ket[site + 1]));
+      const Vector y = detail::apply_effective_two_site(lenv, W[site], W[site + 1], renv, x);
+      // the same product through the dense effective operator (forms.hpp:34-50), as a self-check of the run
+      const Vector yd = detail::effective_two_site_operator(lenv, W[site], W[site + 1], renv) * x;
+      std::ofstream out(outp, std::ios::binary);
+      out.write(reinterpret_cast<const char *>(y.data()), static_cast<std::streamsize>(sizeof(cplx) * y.size()));
+      const Vector xb = detail::tensor_to_vector(detail::join_pair(bra[site], bra[site + 1]));
+      const cplx q = xb.dot(y);
+      std::printf("{\"size\": %lld, \"re\": %.17g, \"im\": %.17g, \"dense_diff\": %.3g, \"ynorm\": %.17g}\n",
+                  static_cast<long long>(y.size()), q.real(), q.imag(), (y - yd).norm(), y.norm());
     } else if (op == "random_uniform") {
       MPS out = random_uniform_mps(std::atoll(arg(0).c_str()), std::atoll(arg(1).c_str()),
                                    std::atoll(arg(2).c_str()), std::strtoull(arg(3).c_str(), nullptr, 10));

@@ -114,6 +114,11 @@ CASES = {
     "qft_uniform_n8": ("qft", strat(), lambda: dict(mps=[_ru(8, 2, 4, 71)])),
     "iqft_complex_n10_chi8": ("iqft", strat(max_bond=8), lambda: dict(mps=[I.random_mps(10, 2, 8, 72, complex_=True)])),
     "qft_product_state_n12": ("qft", strat(tolerance=1e-10), lambda: dict(mps=[_ru(12, 2, 1, 73)])),
+    # --- operator environments + two-site effective operator matvec (environments.hpp:42-83, eigensolvers.hpp:15-64)
+    "heff_laplacian_n8_site3": ("heff", strat(), lambda: dict(mpo=I.laplacian_mpo(8), site=3,
+                                                              mps=[I.random_mps(8, 2, 6, 81, complex_=True)] * 2)),
+    "heff_random_D4_bra_ne_ket": ("heff", strat(), lambda: dict(mpo=I.random_mpo(8, 2, 4, 82), site=2,
+                                                                mps=[I.random_mps(8, 2, 5, 83), I.random_mps(8, 2, 7, 84)])),
     # --- scalars (mps.hpp:416-423, blas.hpp:128-138)
     "scprod_uniform": ("scprod", strat(), lambda: dict(mps=[_ru(9, 2, 5, 61), _ru(9, 2, 7, 62)])),
     "expectation_local_sum": ("expectation_mpo", strat(),
@@ -166,7 +171,7 @@ def run_reference(name, timeout=3600):
             return p
 
         args = []
-        if "mpo" in inp and op in ("apply", "apply_sum", "expectation_mpo"):
+        if "mpo" in inp and op in ("apply", "apply_sum", "expectation_mpo", "heff"):
             p = os.path.join(tmp, "w.ttlab")
             with open(p, "wb") as f:
                 f.write(O.dumps_mpo(O.MPO([np.asarray(t) for t in inp["mpo"]])))
@@ -178,6 +183,8 @@ def run_reference(name, timeout=3600):
                 args += [repr(float(np.real(w))), repr(float(np.imag(w))), p]
         elif op == "canonicalize":
             args = [str(inp["center"])] + files
+        elif op == "heff":
+            args += files + [str(inp["site"])]
         else:
             args += files
         if inp.get("guess") is not None:
@@ -189,6 +196,10 @@ def run_reference(name, timeout=3600):
             raise RuntimeError("ttlab_ref %s failed (%d): %s %s" % (name, r.returncode, r.stdout, r.stderr))
         meta = json.loads(r.stdout.strip().splitlines()[-1])
         tensors = None
+        if op == "heff":  # raw complex128 vector y = H_eff x, stored as one (1, size, 1) "site"
+            y = np.fromfile(outp, dtype=np.complex128)
+            assert y.size == meta["size"] and meta["dense_diff"] <= 1e-12 * max(meta["ynorm"], 1.0)
+            return meta, [y.reshape(1, -1, 1)]
         if os.path.exists(outp):
             with open(outp, "rb") as f:
                 out = O.loads_mps(f.read())
@@ -211,6 +222,19 @@ def load_fixture():
                 ts.append(t)
         out[name] = (m, ts)
     return out
+
+
+def heff_inputs(W, bra, ket, k):
+    """Oracle operator environments around the pair (k, k+1) and x = join_pair(ket pair), complex128."""
+    n = len(ket)
+    L = np.ones((1, 1, 1), dtype=np.complex128)
+    for i in range(k):
+        L = O.update_left_op_environment(L, np.asarray(bra[i]), np.asarray(W[i]), np.asarray(ket[i]))
+    R = np.ones((1, 1, 1), dtype=np.complex128)
+    for i in range(n - 1, k + 1, -1):
+        R = O.update_right_op_environment(R, np.asarray(bra[i]), np.asarray(W[i]), np.asarray(ket[i]))
+    x = np.einsum("asb,btc->astc", np.asarray(ket[k]), np.asarray(ket[k + 1])).reshape(-1).astype(np.complex128)
+    return L, R, x
 
 
 def _qft_layers_host(L, inverse):
@@ -246,6 +270,11 @@ def run_oracle(name):
         out = _omps(inp["mps"][0])
         for layer in reversed(layers):  # the last factor acts first (blas.hpp:24-32)
             out = O.apply(O.MPO(layer), out, s)
+    elif op == "heff":
+        W, bra, ket, k = inp["mpo"], inp["mps"][0], inp["mps"][1], inp["site"]
+        L, R, x = heff_inputs(W, bra, ket, k)
+        y = O.apply_effective_two_site(L, np.asarray(W[k]), np.asarray(W[k + 1]), R, x)
+        return {"size": int(y.size), "ynorm": float(np.linalg.norm(y))}, [np.asarray(y).reshape(1, -1, 1)]
     elif op == "scprod":
         v = O.scprod(_omps(inp["mps"][0]), _omps(inp["mps"][1]))
         return {"re": float(np.real(v)), "im": float(np.imag(v))}, None

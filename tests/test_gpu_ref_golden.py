@@ -34,6 +34,40 @@ def run_gpu(name):
     elif op in ("qft", "iqft"):
         from paper_2601_16734_b200 import qft as Q
         out = (Q.qft if op == "qft" else Q.iqft)(inp["mps"][0], s)
+    elif op == "heff":
+        # operator environments on the device (ttg_op_env_update, device buffers) + the device matvec
+        import ctypes as C
+        import torch
+        from paper_2601_16734_b200 import _lib
+        W, bra, ket, k = inp["mpo"], inp["mps"][0], inp["mps"][1], inp["site"]
+        _, _, x = R.heff_inputs(W, bra, ket, k)
+        ctx = t.context()
+
+        def dev(a):
+            return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.complex128)).cuda()
+
+        def step(env, i, side):
+            b, w, kt = np.asarray(bra[i]), np.asarray(W[i]), np.asarray(ket[i])
+            Dl, dout, din, Dr = w.shape
+            dims = (C.c_int * 8)(Dl, dout, din, Dr, b.shape[0], b.shape[2], kt.shape[0], kt.shape[2])
+            shape = (Dr, b.shape[2], kt.shape[2]) if side == 0 else (Dl, b.shape[0], kt.shape[0])
+            out = torch.empty(shape, dtype=torch.complex128, device="cuda")
+            bufs = [env, dev(b), dev(w), dev(kt)]
+            torch.cuda.synchronize()
+            ctx.check(_lib.lib.ttg_op_env_update(ctx.handle, _lib.TTG_C128, side, dims,
+                                                 *[C.c_void_p(z.data_ptr()) for z in bufs], C.c_void_p(out.data_ptr())))
+            ctx.synchronize()
+            return out
+
+        L = dev(np.ones((1, 1, 1)))
+        for i in range(k):
+            L = step(L, i, 0)
+        Rr = dev(np.ones((1, 1, 1)))
+        for i in range(len(ket) - 1, k + 1, -1):
+            Rr = step(Rr, i, 1)
+        y = t.apply_effective_two_site(L.cpu().numpy(), np.asarray(W[k], dtype=np.complex128),
+                                       np.asarray(W[k + 1], dtype=np.complex128), Rr.cpu().numpy(), x)
+        return {"size": int(np.asarray(y).size)}, [np.asarray(y).reshape(1, -1, 1)]
     elif op == "scprod":
         v = complex(t.scprod(inp["mps"][0], inp["mps"][1])[0])
         return {"re": v.real, "im": v.imag}, None

@@ -22,6 +22,10 @@ ROUNDING_LEVEL = {"simplify_one_site"}
 
 
 def check_against_reference(name, meta, tensors, ref_meta, ref_tensors):
+    if R.CASES[name][0] == "heff":  # y = H_eff x
+        a, b = np.asarray(tensors[0]).ravel(), np.asarray(ref_tensors[0]).ravel()
+        assert a.shape == b.shape and np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b)
+        return
     if ref_tensors is None:  # scalar results
         a, b = complex(meta["re"], meta["im"]), complex(ref_meta["re"], ref_meta["im"])
         assert abs(a - b) <= 1e-12 * max(abs(b), 1.0)
