@@ -71,3 +71,19 @@ struct ChainState {
 enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2, ST_RETRY = 4 };  // ST_RETRY: split pending a jitter retry
 
 }  // namespace ttg
+
+// Debug build switch -DTTG_SMEM_POISON: kernels with a dynamic shared-memory panel start by filling it with NaN
+// bit patterns, so a read of shared memory the kernel did not write shows up at once instead of depending on
+// what the previous kernel on that SM left behind.
+__device__ __forceinline__ void ttg_smem_poison(void* dyn) {
+#ifdef TTG_SMEM_POISON
+  unsigned nbytes;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nbytes));
+  unsigned long long* q = static_cast<unsigned long long*>(dyn);
+  for (unsigned i = threadIdx.x; i < nbytes / 8; i += blockDim.x) q[i] = 0xFFFFFFFFFFFFFFFFull;
+  __syncthreads();
+#else
+  (void)dyn;
+#endif
+}
+

@@ -73,6 +73,7 @@ ttg_status do_svd(int m, int n, const void* theta, int mode, double tol, int64_t
   p.max_bond = max_bond;
   p.mode = mode;
   p.work = work.p;
+  p.s_work = (long long)(m + 1) * (n + 1);  // capacity of `work` in elements (checked by jacobi_svd)
   Buf sw(sizeof(int));
   p.sweeps_out = static_cast<int*>(sw.p);
   p.tol_rot = tol_rot;

@@ -149,6 +149,22 @@ size_t esize(int dtype) { return dtype == TTG_C128 ? 16 : 8; }
 
 // Stream-ordered device allocation (the default pool keeps freed blocks, so
 // repeated calls do not reach cudaMalloc).
+// debug (TTG_WATCH_ADDR=0x..., TTG_WATCH_BYTES=n): checksum of a device range, printed with the split / GEMM traces
+inline void debug_watch(const char* where) {
+  static const unsigned long long addr = getenv("TTG_WATCH_ADDR") ? strtoull(getenv("TTG_WATCH_ADDR"), nullptr, 16) : 0ull;
+  static const size_t nb = getenv("TTG_WATCH_BYTES") ? (size_t)atoll(getenv("TTG_WATCH_BYTES")) : 0;
+  if (!addr || !nb) return;
+  std::vector<double> h(nb / 8);
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(h.data(), reinterpret_cast<const void*>(addr), nb, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();  // range not allocated (yet): nothing to report, no error left behind
+    return;
+  }
+  double a = 0.0;
+  for (double x : h) a += x * x;
+  fprintf(stderr, "    watch %s: %.15e\n", where, std::sqrt(a));
+}
+
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t s = nullptr;
@@ -160,6 +176,12 @@ struct DevBuf {
       cudaGetLastError();
       throw Error{TTG_CAPACITY, "device allocation of " + std::to_string(bytes) + " bytes failed"};
     }
+    // TTG_POISON=1 (debug): every workspace starts as NaN bit patterns, so a read of memory the call did
+    // not write shows up at once instead of depending on what the pool block held before
+    static const bool poison = getenv("TTG_POISON") != nullptr;
+    if (poison) cudaMemsetAsync(p, 0xFF, bytes, st);
+    static const bool dbg_alloc = getenv("TTG_DEBUG_SPLITS") != nullptr;
+    if (dbg_alloc) fprintf(stderr, "  alloc DevBuf %p .. %p (%zu bytes)\n", p, static_cast<char*>(p) + bytes, bytes);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -183,6 +205,10 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
     cudaGetLastError();
     throw Error{TTG_CAPACITY, "device allocation of " + std::to_string(bytes) + " bytes failed"};
   }
+  static const bool poison = getenv("TTG_POISON") != nullptr;  // debug: see DevBuf
+  if (poison) cudaMemsetAsync(p, 0xFF, bytes, s);
+  static const bool dbg_alloc = getenv("TTG_DEBUG_SPLITS") != nullptr;
+  if (dbg_alloc) fprintf(stderr, "  alloc dev %p .. %p (%zu bytes)\n", p, static_cast<char*>(p) + bytes, bytes);
   return p;
 }
 
@@ -293,6 +319,32 @@ struct Engine {
     ProfScope ps(ctx, TTG_PROF_GEMM, flops);
     CK(gemm<T>(p, opA, opB, ub(p.M), ub(p.N), B, st, ub(p.K)));
     ++ctx->launches;
+    static const bool dbg_gemm = getenv("TTG_DEBUG_SPLITS") != nullptr;  // debug: live shape and |C|_F of chain 0
+    if (dbg_gemm) {
+      std::vector<int> hbd(ld);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(hbd.data(), d_bonds, ld * sizeof(int), cudaMemcpyDeviceToHost);
+      const int m = M.eval(hbd.data(), 0, ld), n = N.eval(hbd.data(), 0, ld), k = K.eval(hbd.data(), 0, ld);
+      std::vector<T> hc((size_t)m * n);
+      cudaMemcpy(hc.data(), C, hc.size() * sizeof(T), cudaMemcpyDeviceToHost);
+      double t2 = 0.0;
+      for (auto& x : hc) t2 += abs2(x);
+      std::vector<T> ha((size_t)m * k), hbm((size_t)k * n);
+      cudaMemcpy(ha.data(), A, ha.size() * sizeof(T), cudaMemcpyDeviceToHost);
+      cudaMemcpy(hbm.data(), Bm, hbm.size() * sizeof(T), cudaMemcpyDeviceToHost);
+      double a2 = 0.0, b2 = 0.0, wa = 0.0, wb = 0.0;
+      for (size_t i = 0; i < ha.size(); ++i) {
+        a2 += abs2(ha[i]);
+        wa += abs2(ha[i]) * (double)(i % 97 + 1);
+      }
+      for (size_t i = 0; i < hbm.size(); ++i) {
+        b2 += abs2(hbm[i]);
+        wb += abs2(hbm[i]) * (double)(i % 89 + 1);
+      }
+      debug_watch("after gemm");
+      fprintf(stderr, "  gemm op %d %d live %d x %d x %d (bounds %d %d %d) |C| %.15e |A| %.12e (%.12e) |B| %.12e (%.12e) A %p B %p C %p\n",
+              opA, opB, m, n, k, ub(p.M), ub(p.N), ub(p.K), std::sqrt(t2), std::sqrt(a2), wa, std::sqrt(b2), wb, A, Bm, C);
+    }
   }
 
   struct Warm {
@@ -327,6 +379,83 @@ struct Engine {
         e->invalidate_bond(e->pre_slot);
       }
     } inval{this, out_idx};
+    // TTG_DEBUG_SPLITS=1: one line per split on stderr (bounds, live shape, resulting rank of chain 0)
+    static const bool dbg_splits = getenv("TTG_DEBUG_SPLITS") != nullptr;
+    struct DbgSplit {
+      Engine* e;
+      DimExpr M, N;
+      int idx, mode, pre;
+      bool on;
+      int m = 0, n = 0;
+      void live(int& a, int& b, int& r) {
+        std::vector<int> hb(e->ld);
+        cudaStreamSynchronize(e->st);
+        cudaMemcpy(hb.data(), e->d_bonds, e->ld * sizeof(int), cudaMemcpyDeviceToHost);
+        a = M.eval(hb.data(), 0, e->ld);
+        b = N.eval(hb.data(), 0, e->ld);
+        r = hb[idx];
+      }
+      DbgSplit(Engine* e_, DimExpr M_, DimExpr N_, int idx_, int mode_, int pre_, bool on_)
+          : e(e_), M(M_), N(N_), idx(idx_), mode(mode_), pre(pre_), on(on_) {
+        int r;
+        if (on) live(m, n, r);
+      }
+      const void* theta = nullptr;
+      const void* iso = nullptr;
+      ~DbgSplit() {
+        if (!on) return;
+        int a, b, r;
+        live(a, b, r);
+        // |theta|_F and the orthonormality defect of the isometry (chain 0), computed on the host
+        double tn = 0.0, defect = 0.0;
+        {
+          std::vector<T> th((size_t)m * n), is((size_t)(mode == 0 ? m : n) * r);
+          cudaMemcpy(th.data(), theta, th.size() * sizeof(T), cudaMemcpyDeviceToHost);
+          cudaMemcpy(is.data(), iso, is.size() * sizeof(T), cudaMemcpyDeviceToHost);
+          for (auto& x : th) tn += abs2(x);
+          const int len = mode == 0 ? m : n;  // mode 0: iso is len x r (columns); mode 1: r x len (rows)
+          for (int p = 0; p < r; ++p)
+            for (int q = 0; q < r; ++q) {
+              double gr = 0.0, gi = 0.0;
+              for (int i = 0; i < len; ++i) {
+                const T u = mode == 0 ? is[(size_t)i * r + p] : is[(size_t)p * len + i];
+                const T v = mode == 0 ? is[(size_t)i * r + q] : is[(size_t)q * len + i];
+                if constexpr (Scalar<T>::is_complex) {
+                  gr += u.x * v.x + u.y * v.y;
+                  gi += u.x * v.y - u.y * v.x;
+                } else {
+                  gr += u * v;
+                }
+              }
+              defect = std::max(defect, std::hypot(gr - (p == q ? 1.0 : 0.0), gi));
+            }
+          // weight of theta outside the span of the isometry: |theta|^2 - |U^H theta|^2 (mode 0) or - |theta V|^2
+          double kept = 0.0;
+          for (int p = 0; p < r; ++p)
+            for (int j = 0; j < (mode == 0 ? n : m); ++j) {
+              double gr = 0.0, gi = 0.0;
+              for (int i = 0; i < len; ++i) {
+                const T u = mode == 0 ? is[(size_t)i * r + p] : is[(size_t)p * len + i];
+                const T x = mode == 0 ? th[(size_t)i * n + j] : th[(size_t)j * n + i];
+                if constexpr (Scalar<T>::is_complex) {
+                  // mode 0: conj(u) x; mode 1: x conj(v^H row) = x * conj(u)
+                  gr += u.x * x.x + u.y * x.y;
+                  gi += u.x * x.y - u.y * x.x;
+                } else {
+                  gr += u * x;
+                }
+              }
+              kept += gr * gr + gi * gi;
+            }
+          fprintf(stderr, "   outside weight %.6e of |theta|^2 %.6e\n", tn - kept, tn);
+        }
+        debug_watch("after split");
+        fprintf(stderr, "split mode %d no_pre %d bounds %d x %d live %d x %d -> bond[%d] = %d  |theta| %.15e iso defect %.2e\n",
+                mode, pre, e->ub(M), e->ub(N), m, n, idx, r, std::sqrt(tn), defect);
+      }
+    } dbg_split(this, M, N, out_idx, mode, no_pre ? 1 : 0, dbg_splits);
+    dbg_split.theta = theta;
+    dbg_split.iso = iso;
     SvdParams p{};
     static const int no_early = [] {
       const char* e = getenv("TTG_SVD_EARLY");
@@ -470,6 +599,18 @@ void Engine<T>::split_preconditioned(const void* theta, long long s_theta, DimEx
   const DimExpr Kc = mode == 0 ? N : M;  // number of columns k
   const DimExpr R0 = dbond(pre_slot);
   const int lu = ub(Lr), ku = ub(Kc);
+  // The preconditioner rank r0 <= min(l, k) of THIS split: the inner split below sizes its kernel (panel in
+  // shared memory or in the global workspace) from the bound of the rank slot, which otherwise is the largest
+  // d * bond of the whole chain.  With that loose bound a 32 x 32 inner split of a chain with one 256-wide
+  // bond elsewhere chose the global-workspace kernel although the plan (sized from the outer shapes, which do
+  // fit shared memory) had reserved no workspace: its panel overran the 16-byte placeholder into neighbouring
+  // allocations (found by tools/fuzz_parity.py: results depended on what the pool had placed there).
+  struct BoundGuard {
+    std::vector<int>& b;
+    int idx, saved;
+    BoundGuard(std::vector<int>& b_, int idx_, int v) : b(b_), idx(idx_), saved(b_[idx_]) { b[idx] = std::min(saved, v); }
+    ~BoundGuard() { b[idx] = saved; }
+  } rank_bound(bound, pre_slot, std::min(lu, ku));
   const ChainState* stp = check_active ? d_state : nullptr;
   double qflops = 0.0;  // QR with Q: 4n^2(m - n/3); R only: 2n^2(m - n/3)
   if (live_dims(check_active))
@@ -886,8 +1027,8 @@ void run_simplify(ttg_ctx* ctx, const ttg_dmps& target, const ttg_dmps& guess, c
   for (int n = 0; n + 1 < L; ++n) {
     const long long side = std::max((long long)pb[n] * d[n], (long long)d[n + 1] * pb[n + 2]);
     fcap[n] = side * side;
-    frameU.emplace_back((size_t)B * fcap[n] * es, st);
-    frameV.emplace_back((size_t)B * fcap[n] * es, st);
+    frameU.emplace_back(warm_frames ? (size_t)B * fcap[n] * es : 0, st);  // placeholders unless TTG_SVD_WARM=1
+    frameV.emplace_back(warm_frames ? (size_t)B * fcap[n] * es : 0, st);
   }
   DevBuf fmeta((size_t)2 * B * L * sizeof(int), st);
   CK(cudaMemsetAsync(fmeta.p, 0, (size_t)2 * B * L * sizeof(int), st));

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_kernel(QrParams p, int in_smem)
   __shared__ T s_tau;
   const int chain = blockIdx.x;
   const int m = p.m, n = p.n, k = min(m, n);
+  ttg_smem_poison(smem_raw);
   T* Wk = in_smem ? reinterpret_cast<T*>(smem_raw) : static_cast<T*>(p.work) + p.s_work * chain;
   T* E = Wk + (size_t)m * n;
   T* tau = E + (size_t)m * k;
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_r_kernel(const T* A, long long 
   __shared__ T s_tau;
   const int chain = blockIdx.x;
   const int m = M.eval(bonds, chain, ld), n = N.eval(bonds, chain, ld);
+  ttg_smem_poison(smem_raw);
   A += sA * chain;
   R += sR * chain;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_pre_kernel(const T* A, long lon
   __shared__ T taus[1024];
   const int chain = blockIdx.x;
   if (st && !st[chain].active) return;
+  ttg_smem_poison(smem_raw);
   const int mi = Md.eval(bonds, chain, ld), ni = Nd.eval(bonds, chain, ld);
   const bool out_r = (trans & 2) != 0;  // write R (r0 x k) instead of R^H
   trans &= 1;

@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(QRS_THREADS, 1)
   __shared__ double red[Scalar<T>::is_complex ? 2 * NB : NB];
   const int chain = blockIdx.x;
   if (st && !st[chain].active) return;
+  ttg_smem_poison(smem_raw);
   const int mi = Md.eval(bonds, chain, ld), ni = Nd.eval(bonds, chain, ld);
   const bool out_r = (trans & 2) != 0;  // write R (r0 x k) instead of R^H
   trans &= 1;

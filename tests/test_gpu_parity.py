@@ -338,3 +338,41 @@ def test_expectations():
     got = t.expectation_mpo(W, psi)[0]
     ref = O.expectation_mpo(O.MPO(W), omps(psi))
     assert abs(got - ref) <= 1e-12 * max(abs(ref), 1.0)
+
+
+@pytest.mark.parametrize("name", ["s2_223", "s2_521", "s3_519"])
+def test_fuzz_regression_inner_split_workspace(name):
+    """Cases found by tools/fuzz_parity.py (complex chains with mixed physical dimensions, tolerance-only
+    truncation): the rank-revealing preconditioner's inner split sized its kernel from the loosest bond bound
+    of the chain, picked the global-workspace kernel although no workspace had been planned, and its panel
+    overran a 16-byte placeholder into whatever the pool had placed behind it (here: a target site tensor), so
+    results depended on allocator history.  Now the rank bound is per split and an undersized workspace is an
+    error; these inputs must simply match the oracle."""
+    import json
+    t = T()
+    z = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "fuzz_regressions.npz"))
+    meta = json.loads(str(z["meta"]))[name]
+    a = [z[f"{name}/a/{i}"] for i in range(meta["a"])]
+    b = [z[f"{name}/b/{i}"] for i in range(meta["b"])] if "b" in meta else None
+    kw = dict(method=meta["method"], tolerance=meta["tolerance"], max_sweeps=meta["max_sweeps"],
+              normalize=meta["normalize"])
+    so = O.Strategy(max_bond=meta["max_bond"] or O.UNBOUNDED_BOND, **kw)
+    sg = t.Strategy(max_bond=meta["max_bond"] or t.UNBOUNDED_BOND, **kw)
+    # a small complex sum first: the call whose workspaces, once freed, the original failure needed behind its own
+    w = [(-0.86 - 0.54j), 0.29, -1.6]
+    pre = [I.random_mps(4, 2, 3, 900 + i) for i in range(3)]
+    t.simplify(t.MPSSum(w, pre), t.Strategy(max_bond=2, max_sweeps=2))
+    for _ in range(2):
+        if b is None:
+            ref = O.simplify(omps(a), so)
+            got = t.simplify(a, sg)
+        else:
+            ref = O.simplify(O.hadamard(omps(a), omps(b)), so)
+            got = t.simplify(t.hadamard(a, b), sg)
+        ts = got.to_tensors()
+        assert [x.shape for x in ts] == [x.shape for x in ref.tensors]
+        assert distance(ts, ref.tensors) <= 1e-10 * ref.norm()
+        # exact-fit targets: residual^2 = <T,T> - |psi|^2 is cancellation noise of order eps <T,T>
+        scale = max(ref.norm(), ref.error)
+        assert (abs(got.error() - ref.error) <= 1e-10 * scale
+                or abs(got.error() ** 2 - ref.error ** 2) <= 1e-13 * scale ** 2)

@@ -1,0 +1,214 @@
+"""Randomised parity sweep: the CUDA path against the oracle on many small seeded cases.
+
+    python tools/fuzz_parity.py [cases] [seed] [big]
+
+Draws (op, chain length, physical dimensions — mixed per site —, bonds, dtype, strategy) at random and
+compares bond dimensions, norm, error ledger and the cancellation-free distance of the outputs
+(tests/_compare.py), with the tolerances of tests/test_oracle_vs_ref.py.  Prints every failing case with
+its parameters; exit status 1 if any failed.  Not part of the pytest suite (minutes of oracle time)."""
+import sys
+import time
+import traceback
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from oracle import ttlab_oracle as O  # noqa: E402
+from paper_2601_16734_b200 import ttlab as t  # noqa: E402
+from tests._compare import distance  # noqa: E402
+
+
+BIG = len(sys.argv) > 3 and sys.argv[3] == "big"  # third argument "big": chains to 12 sites, bonds to 71
+
+
+def rand_mps(rng, dims, chi, cplx):
+    n = len(dims)
+    bonds = [1]
+    for k in range(1, n):
+        left = int(np.prod(dims[:k], dtype=object))
+        right = int(np.prod(dims[k:], dtype=object))
+        bonds.append(max(1, min(chi, left, right)))
+    bonds.append(1)
+    ts = []
+    for k in range(n):
+        x = rng.standard_normal((bonds[k], dims[k], bonds[k + 1]))
+        if cplx:
+            x = x + 1j * rng.standard_normal(x.shape)
+        ts.append(x / np.sqrt(x.size) * 2.0)
+    return ts
+
+
+def rand_mpo(rng, dims, D, cplx):
+    n = len(dims)
+    ws = []
+    for k in range(n):
+        l = 1 if k == 0 else D
+        r = 1 if k == n - 1 else D
+        x = rng.standard_normal((l, dims[k], dims[k], r))
+        if cplx:
+            x = x + 1j * rng.standard_normal(x.shape)
+        ws.append(x / np.sqrt(dims[k] * max(l, r)))
+    return ws
+
+
+def strategies(rng):
+    method = O.VARIATIONAL if rng.random() < 0.75 else O.SVD_TRUNCATE
+    tol = float(rng.choice([1e-12, 1e-12, 1e-8, 1e-4, 1e-2]))
+    mb = int(rng.integers(1, 40 if BIG else 14)) if rng.random() < 0.7 else 0
+    kw = dict(method=method, tolerance=tol, max_sweeps=int(rng.integers(1, 5)), normalize=bool(rng.random() < 0.2))
+    o = O.Strategy(max_bond=mb or O.UNBOUNDED_BOND, **kw)
+    g = t.Strategy(max_bond=mb or t.UNBOUNDED_BOND, **kw)
+    return o, g, dict(kw, max_bond=mb)
+
+
+KNIFE = []  # cases whose only difference is a stop-rule knife edge (see one_case)
+rng_floor = np.random.default_rng(12345)
+SKIP = [False]  # FUZZ_FROM / FUZZ_TO: cases outside the window only draw their inputs
+DUMP = {}  # inputs of the case being run (written next to the log when it fails)
+
+
+def one_case(rng):
+    DUMP.clear()
+    op = str(rng.choice(["simplify", "apply", "hadamard", "canonicalize", "sum", "apply_sum"]))
+    n = int(rng.integers(1, 13 if BIG else 10))
+    dims = [int(rng.choice([2, 2, 2, 3, 4])) for _ in range(n)]
+    cplx = bool(rng.random() < 0.4)
+    chi = int(rng.integers(1, 72 if BIG else 20))
+    so, sg, sdesc = strategies(rng)
+    desc = dict(op=op, dims=dims, cplx=cplx, chi=chi, **sdesc)
+    om = lambda ts: O.MPS([np.asarray(x) for x in ts], 0.0)  # noqa: E731
+    if op == "simplify":
+        a = rand_mps(rng, dims, chi, cplx)
+        DUMP.update(a=a)
+        run_ref, run_gpu = (lambda: O.simplify(om(a), so)), (lambda: t.simplify(a, sg))
+    elif op == "apply":
+        a = rand_mps(rng, dims, min(chi, 8), cplx)
+        W = rand_mpo(rng, dims, int(rng.integers(1, 4)), cplx and rng.random() < 0.5)
+        DUMP.update(a=a, W=W)
+        run_ref, run_gpu = (lambda: O.apply(O.MPO(W), om(a), so)), (lambda: t.apply(W, a, sg))
+    elif op == "hadamard":
+        a, b = rand_mps(rng, dims, min(chi, 5), cplx), rand_mps(rng, dims, min(chi, 4), cplx)
+        DUMP.update(a=a, b=b)
+        run_ref = lambda: O.simplify(O.hadamard(om(a), om(b)), so)  # noqa: E731
+        run_gpu = lambda: t.simplify(t.hadamard(a, b), sg)  # noqa: E731
+    elif op == "canonicalize":
+        a = rand_mps(rng, dims, chi, cplx)
+        DUMP.update(a=a)
+        c = int(rng.integers(0, n))
+        desc["center"] = c
+        run_ref, run_gpu = (lambda: O.canonicalize(om(a), c, so)), (lambda: t.canonicalize(a, c, sg))
+    else:
+        terms = int(rng.integers(2, 4))
+        states = [rand_mps(rng, dims, int(rng.integers(1, 7)), cplx) for _ in range(terms)]
+        w = [complex(rng.standard_normal(), rng.standard_normal() if rng.random() < 0.5 else 0.0) for _ in range(terms)]
+        desc["weights"] = w
+        DUMP.update(states=states)
+        W = rand_mpo(rng, dims, int(rng.integers(1, 3)), False) if op == "apply_sum" else None
+        if op == "sum":
+            run_ref = lambda: O.simplify_sum(O.MPSSum(w, [om(s) for s in states]), so)  # noqa: E731
+            run_gpu = lambda: t.simplify(t.MPSSum(w, states), sg)  # noqa: E731
+        else:
+            run_ref = lambda: O.apply_sum(O.MPO(W), O.MPSSum(w, [om(s) for s in states]), so)  # noqa: E731
+            run_gpu = lambda: t.apply(W, t.MPSSum(w, states), sg)  # noqa: E731
+    def run_ref_perturbed(f):
+        saved = {}
+        for key in ("a", "b"):
+            if key in DUMP:
+                saved[key] = DUMP[key][0].copy()
+                DUMP[key][0] *= f
+        for st_ in DUMP.get("states", []):
+            saved[id(st_)] = st_[0].copy()
+            st_[0] *= f
+        try:
+            return run_ref()
+        finally:
+            for key in ("a", "b"):
+                if key in saved:
+                    DUMP[key][0][...] = saved[key]
+            for st_ in DUMP.get("states", []):
+                st_[0][...] = saved[id(st_)]
+
+    if SKIP[0]:  # inputs drawn (the random stream stays aligned), nothing run
+        return desc, []
+    try:
+        ref = run_ref()
+    except O.ShapeError as e:
+        # e.g. one-site sums with SVD_TRUNCATE: MPSSum::join builds a (1, d, terms) tensor and the MPS
+        # constructor rejects it (mps.hpp:369-372, 28-30): the device path must raise the same error
+        desc["oracle_raises"] = str(e)
+        try:
+            run_gpu()
+        except t.ShapeError:
+            return desc, []
+        return desc, ["oracle raised ShapeError, the device path did not"]
+    got = run_gpu()
+    ts = got.to_tensors()
+    DUMP.update(gpu=ts, ref=ref.tensors)
+    rb, gb = [x.shape[2] for x in ref.tensors], [x.shape[2] for x in ts]
+    problems = []
+    nrm = ref.norm()
+    gn = float(t.norm(got)[0])
+    scale = max(nrm, ref.error, 1e-300)
+    if rb != gb:
+        problems.append(f"bonds {gb} != {rb}")
+    else:
+        d = distance(ts, ref.tensors)
+        if not d <= 1e-10 * max(nrm, 1e-300) + 1e-14:
+            # The stop rules of the sweeps (simplify.hpp:118-124) compare quantities at cancellation level, so a
+            # last-bit change can end the run one sweep earlier or later and move the output by ~1e-10 |psi|: the
+            # oracle itself jumps by the same amount under 1-ulp perturbations of its input.  Such cases are
+            # reported as knife edges, not as failures.
+            floors = []
+            for _ in range(6):
+                scale_in = 1.0 + 2.2e-16 * rng_floor.standard_normal()
+                try:
+                    alt = run_ref_perturbed(scale_in)
+                    if [x.shape for x in alt.tensors] == [x.shape for x in ref.tensors]:
+                        floors.append(distance(alt.tensors, ref.tensors))
+                except Exception:  # noqa: BLE001
+                    pass
+            if floors and max(floors) >= 0.5 * d:
+                desc["knife_edge"] = f"oracle moves {max(floors):.2e} under a 1-ulp input scaling; device {d:.2e}"
+                KNIFE.append(desc)
+            else:
+                problems.append(f"distance {d:.3e} vs norm {nrm:.3e} (oracle noise floor {max(floors or [0]):.1e})")
+    if not abs(gn - nrm) <= 1e-10 * max(nrm, 1e-300) + 1e-14:
+        problems.append(f"norm {gn!r} != {nrm!r}")
+    ge = float(got.error())
+    if not (abs(ge - ref.error) <= 1e-10 * scale or abs(ge ** 2 - ref.error ** 2) <= 1e-13 * scale ** 2):
+        problems.append(f"error {ge!r} != {ref.error!r}")
+    return desc, problems
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    rng = np.random.default_rng(seed)
+    bad = 0
+    t0 = time.time()
+    import os
+    lo, hi = int(os.environ.get("FUZZ_FROM", 0)), int(os.environ.get("FUZZ_TO", cases))
+    for i in range(cases):
+        SKIP[0] = not (lo <= i <= hi)
+        state = rng.bit_generator.state
+        try:
+            desc, problems = one_case(rng)
+        except Exception:  # noqa: BLE001
+            desc, problems = {"rng_state": state["state"]}, ["exception: " + traceback.format_exc(limit=3)]
+        if problems:
+            bad += 1
+            import os
+            import pickle
+            os.makedirs("gpurun_out", exist_ok=True)
+            with open(f"gpurun_out/fuzz_fail_s{seed}{'b' if BIG else ''}_{i}.pkl", "wb") as f:
+                pickle.dump(dict(desc=desc, problems=problems, **DUMP), f)
+            print(f"FAIL case {i}: {desc}\n     " + "; ".join(problems), flush=True)
+    for kd in KNIFE:
+        print(f"knife edge: {kd}")
+    print(f"{cases - bad} / {cases} cases agree, {len(KNIFE)} of them on a stop-rule knife edge "
+          f"({time.time() - t0:.0f} s, seed {seed})")
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
