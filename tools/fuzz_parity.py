@@ -18,7 +18,8 @@ from paper_2601_16734_b200 import ttlab as t  # noqa: E402
 from tests._compare import distance  # noqa: E402
 
 
-BIG = len(sys.argv) > 3 and sys.argv[3] == "big"  # third argument "big": chains to 12 sites, bonds to 71
+BIG = len(sys.argv) > 3 and sys.argv[3] in ("big", "huge")  # "big": chains to 12 sites, bonds to 71
+HUGE = len(sys.argv) > 3 and sys.argv[3] == "huge"  # "huge": bonds to 320 (grid / cluster kernels, blocked QR)
 
 
 def rand_mps(rng, dims, chi, cplx):
@@ -54,7 +55,7 @@ def rand_mpo(rng, dims, D, cplx):
 def strategies(rng):
     method = O.VARIATIONAL if rng.random() < 0.75 else O.SVD_TRUNCATE
     tol = float(rng.choice([1e-12, 1e-12, 1e-8, 1e-4, 1e-2]))
-    mb = int(rng.integers(1, 40 if BIG else 14)) if rng.random() < 0.7 else 0
+    mb = int(rng.integers(1, (200 if HUGE else 40) if BIG else 14)) if rng.random() < 0.7 else 0
     kw = dict(method=method, tolerance=tol, max_sweeps=int(rng.integers(1, 5)), normalize=bool(rng.random() < 0.2))
     o = O.Strategy(max_bond=mb or O.UNBOUNDED_BOND, **kw)
     g = t.Strategy(max_bond=mb or t.UNBOUNDED_BOND, **kw)
@@ -69,14 +70,41 @@ DUMP = {}  # inputs of the case being run (written next to the log when it fails
 
 def one_case(rng):
     DUMP.clear()
-    op = str(rng.choice(["simplify", "apply", "hadamard", "canonicalize", "sum", "apply_sum"]))
+    op = str(rng.choice(["simplify", "apply", "hadamard", "canonicalize", "sum", "apply_sum", "batch"]))
     n = int(rng.integers(1, 13 if BIG else 10))
     dims = [int(rng.choice([2, 2, 2, 3, 4])) for _ in range(n)]
     cplx = bool(rng.random() < 0.4)
     chi = int(rng.integers(1, 72 if BIG else 20))
+    if HUGE:
+        n = int(rng.integers(8, 12))
+        dims = [int(rng.choice([2, 3, 4, 4])) for _ in range(n)]
+        chi = int(rng.integers(40, 200))
     so, sg, sdesc = strategies(rng)
     desc = dict(op=op, dims=dims, cplx=cplx, chi=chi, **sdesc)
     om = lambda ts: O.MPS([np.asarray(x) for x in ts], 0.0)  # noqa: E731
+    if op == "batch":  # several chains of one shape through the batched engine, each against its own oracle run
+        nb = int(rng.integers(2, 7))
+        chains = [rand_mps(rng, dims, min(chi, 24), cplx) for _ in range(nb)]
+        so = so.with_normalize(False)
+        sg = sg.with_normalize(False)
+        if SKIP[0]:
+            return desc, []
+        refs = [O.simplify(om(c), so) for c in chains]
+        got = t.simplify(t.DeviceMPS.from_batch(chains), sg)
+        problems = []
+        for i, ref in enumerate(refs):
+            ts = got.to_tensors(i)
+            if [x.shape for x in ts] != [x.shape for x in ref.tensors]:
+                problems.append(f"chain {i}: bonds differ")
+                continue
+            dd = distance(ts, ref.tensors)
+            if not dd <= 3e-10 * max(ref.norm(), 1e-300) + 1e-14:  # 3e-10: room for the stop-rule knife edge
+                problems.append(f"chain {i}: distance {dd:.3e} vs norm {ref.norm():.3e}")
+            ge = float(got.error(i))
+            sc = max(ref.norm(), ref.error, 1e-300)
+            if not (abs(ge - ref.error) <= 3e-10 * sc or abs(ge ** 2 - ref.error ** 2) <= 1e-13 * sc ** 2):
+                problems.append(f"chain {i}: error {ge!r} != {ref.error!r}")
+        return desc, problems
     if op == "simplify":
         a = rand_mps(rng, dims, chi, cplx)
         DUMP.update(a=a)
