@@ -327,6 +327,30 @@ def test_svd_clustered_spectrum_isometry(n, seed, svd_impl):
         assert np.abs(sv - np.sort(s)[::-1]).max() < 1e-13
 
 
+@pytest.mark.parametrize("shape", [(47, 6), (5, 64), (66, 9), (112, 113), (75, 258), (182, 147), (319, 141)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_svd_clustered_spectrum_isometry_complex(shape, mode):
+    """Complex splits with clustered singular values (sigma = 1 +- 1e-9) on the shapes tools/fuzz_split.py
+    caught: the register-blocked one-CTA kernel stopped early without the guards of the ring kernels and left
+    |U^H U - I| up to 9e-10."""
+    m, n = shape
+    k = min(m, n)
+    rng = np.random.default_rng(m * 1000 + n)
+    U, _ = np.linalg.qr(rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)))
+    s = np.sort(1.0 + 1e-9 * rng.standard_normal(k))[::-1]
+    th = (U * s) @ V.conj().T
+    iso, sv, r, _ = _svd(th, mode, tol=1e-12)
+    assert r == k
+    if mode == 0:
+        assert np.abs(iso.conj().T @ iso - np.eye(r)).max() < 1e-12
+        assert np.abs(iso @ (iso.conj().T @ th) - th).max() < 1e-11
+    else:
+        assert np.abs(iso @ iso.conj().T - np.eye(r)).max() < 1e-12
+        assert np.abs((th @ iso.conj().T) @ iso - th).max() < 1e-11
+    assert np.abs(sv - s).max() < 1e-13
+
+
 _RETRY_SNIPPET = r'''
 import sys, numpy as np
 sys.path.insert(0, ".")
