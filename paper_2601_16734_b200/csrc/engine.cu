@@ -2531,7 +2531,11 @@ void heff_two_site_dev(ttg_ctx* ctx, const int* dm, const void* L, const void* W
     CK(gemm<T>(g1, OP_N, OP_N, M1, N1, 1, st, chiA));
   }
   const size_t smem = (size_t)D0 * d1o * d1 * d2o * d2 * D2 * es;  // fused W12
-  if (smem > 48 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
+  // the fused pair W12 lives in shared memory: up to 200 KB (e.g. D = 8 with d = 4 on both sites: 8 * 16 * 16 * 8
+  // complex values = 256 KB does not fit; D = 4, d = 4: 64 KB does)
+  if (smem > 200 * 1024) throw Error{TTG_CAPACITY, "apply_effective_two_site: MPO sites too large"};
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(heff_mix_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   (void)nW1;
   (void)nW2;
   const long long tot = (long long)chiAo * chiB;

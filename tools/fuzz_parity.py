@@ -73,7 +73,7 @@ def one_case(rng):
     DUMP.clear()
     REP_O.clear()
     REP_G.clear()
-    op = str(rng.choice(["simplify", "apply", "hadamard", "canonicalize", "sum", "apply_sum", "batch"]))
+    op = str(rng.choice(["simplify", "apply", "hadamard", "canonicalize", "sum", "apply_sum", "batch", "qft"]))
     n = int(rng.integers(1, 13 if BIG else 10))
     dims = [int(rng.choice([2, 2, 2, 3, 4])) for _ in range(n)]
     cplx = bool(rng.random() < 0.4)
@@ -85,6 +85,33 @@ def one_case(rng):
     so, sg, sdesc = strategies(rng)
     desc = dict(op=op, dims=dims, cplx=cplx, chi=chi, **sdesc)
     om = lambda ts: O.MPS([np.asarray(x) for x in ts], 0.0)  # noqa: E731
+    if op == "qft":  # MPO list: the Fourier circuit layer by layer (qft.hpp:68-113, blas.hpp:24-32), qubits only
+        from paper_2601_16734_b200 import qft as Q
+        n = min(n, 9)
+        dims = [2] * n
+        inverse = bool(rng.random() < 0.5)
+        a = rand_mps(rng, dims, min(chi, 12), cplx)
+        desc.update(dims=dims, inverse=inverse)
+        if SKIP[0]:
+            return desc, []
+        sign = 1.0 if inverse else -1.0
+        order = range(n) if inverse else range(n - 1, -1, -1)
+        layers = [Q.qft_layer(n, list(range(n)), m_, sign, inverse) for m_ in order]
+        ref = om(a)
+        for layer in reversed(layers):
+            ref = O.apply(O.MPO(layer), ref, so)
+        got = (Q.iqft if inverse else Q.qft)(a, sg)
+        ts = got.to_tensors()
+        if [x.shape for x in ts] != [x.shape for x in ref.tensors]:
+            return desc, ["bonds differ"]
+        dd = distance(ts, ref.tensors)
+        # n layers, each with its own stop-rule knife edge and its own sqrt(eps) ledger noise when it fits exactly
+        if not dd <= 1e-9 * max(ref.norm(), 1e-300) + 1e-14:
+            return desc, [f"distance {dd:.3e} vs norm {ref.norm():.3e}"]
+        sc = max(ref.norm(), ref.error, 1e-300)
+        if abs(float(got.error()) - ref.error) > n * 3.2e-7 * sc:
+            return desc, [f"error {got.error()!r} != {ref.error!r}"]
+        return desc, []
     if op == "batch":  # several chains of one shape through the batched engine, each against its own oracle run
         nb = int(rng.integers(2, 7))
         chains = [rand_mps(rng, dims, min(chi, 24), cplx) for _ in range(nb)]

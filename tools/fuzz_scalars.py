@@ -22,7 +22,7 @@ om = lambda ts: O.MPS([np.asarray(x) for x in ts], 0.0)  # noqa: E731
 bad = 0
 t0 = time.time()
 for i in range(cases):
-    op = str(rng.choice(["scprod", "norm", "expectation_mpo", "expectation_local", "recenter"]))
+    op = str(rng.choice(["scprod", "norm", "expectation_mpo", "expectation_local", "recenter", "heff"]))
     n = int(rng.integers(1, 11))
     dims = [int(rng.choice([2, 2, 3, 4])) for _ in range(n)]
     cu, cv, cw = (bool(rng.random() < 0.4) for _ in range(3))
@@ -61,6 +61,24 @@ for i in range(cases):
             sc = max(om(u).norm() ** 2, 1e-300) * 10.0
             if abs(got - ref) > 1e-11 * sc:
                 problems.append(f"{got} != {ref}")
+        elif op == "heff":  # y = H_eff x around a random pair, bra != ket (eigensolvers.hpp:15-64)
+            if n < 2:
+                continue
+            W = rand_mpo(rng, dims, int(rng.integers(1, 5)), cw)
+            k = int(rng.integers(0, n - 1))
+            desc.update(site=k, D=int(np.asarray(W[k]).shape[3]))
+            cp = lambda a: np.asarray(a, dtype=np.complex128)  # noqa: E731
+            L = np.ones((1, 1, 1), dtype=np.complex128)
+            for j in range(k):
+                L = O.update_left_op_environment(L, cp(u[j]), cp(W[j]), cp(v[j]))
+            R = np.ones((1, 1, 1), dtype=np.complex128)
+            for j in range(n - 1, k + 1, -1):
+                R = O.update_right_op_environment(R, cp(u[j]), cp(W[j]), cp(v[j]))
+            x = np.einsum("asb,btc->astc", cp(v[k]), cp(v[k + 1])).reshape(-1)
+            ref = O.apply_effective_two_site(L, cp(W[k]), cp(W[k + 1]), R, x)
+            got = np.asarray(t.apply_effective_two_site(L, cp(W[k]), cp(W[k + 1]), R, x)).reshape(-1)
+            if got.shape != ref.reshape(-1).shape or np.linalg.norm(got - ref.reshape(-1)) > 1e-11 * max(np.linalg.norm(ref), 1e-300):
+                problems.append(f"|y - y_ref| {np.linalg.norm(got - ref.reshape(-1)):.2e} of {np.linalg.norm(ref):.2e}")
         else:  # canonicalize, then move the centre with truncation (mps.hpp:268-279)
             c0, c1 = int(rng.integers(0, n)), int(rng.integers(0, n))
             mb = int(rng.integers(1, 20))
