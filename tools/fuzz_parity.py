@@ -81,7 +81,8 @@ def one_case(rng):
     if HUGE:
         n = int(rng.integers(8, 12))
         dims = [int(rng.choice([2, 3, 4, 4])) for _ in range(n)]
-        chi = int(rng.integers(40, 200))
+        import os as _os
+        chi = int(rng.integers(40, int(_os.environ.get("FUZZ_CHI_MAX", 200))))
     so, sg, sdesc = strategies(rng)
     desc = dict(op=op, dims=dims, cplx=cplx, chi=chi, **sdesc)
     om = lambda ts: O.MPS([np.asarray(x) for x in ts], 0.0)  # noqa: E731

@@ -3,7 +3,8 @@ selected by shape): random m x n up to 320 (with a bias to odd and tiny sizes), 
 random tolerance and max_bond, graded and rank-deficient spectra.  Checked against numpy's SVD: rank rule
 (schmidt.hpp:40-59), dropped weight, |theta - a b| = dropped weight, isometry of the orthonormal factor.
 
-    python tools/fuzz_split.py [cases] [seed]"""
+    python tools/fuzz_split.py [cases] [seed] [big]      ("big": 200 .. 1600 rows / columns, the grid, cluster,
+                                                          block-Gram and blocked-QR paths at odd sizes)"""
 import sys
 import time
 
@@ -17,11 +18,16 @@ seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 rng = np.random.default_rng(seed)
 bad = 0
 t0 = time.time()
+BIG = len(sys.argv) > 3 and sys.argv[3] == "big"
 for i in range(cases):
     big = rng.random() < 0.25
     m = int(rng.integers(1, 320 if big else 70))
     n = int(rng.integers(1, 320 if big else 70))
     cplx = rng.random() < 0.4
+    if BIG:
+        cplx = rng.random() < 0.3
+        top = 1000 if cplx else 1600
+        m, n = int(rng.integers(200, top)), int(rng.integers(200, top))
     kind = str(rng.choice(["gauss", "graded", "lowrank", "clustered"]))
     k = min(m, n)
 
